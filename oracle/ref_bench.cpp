@@ -1,0 +1,109 @@
+// CPU baseline driver. TEST/BENCH INFRASTRUCTURE ONLY.
+//
+// Times the reference's own fitness path (Engine::sanity_check semantics:
+// validate + evaluate_fitness, src/engine.cpp:91-95 and src/vm.cpp:558-579)
+// over a workload of variants, on the host cores, with a plain std::thread
+// pool (the reference's parallel_for shape, src/engine.cpp:28-62). Used by
+// bench.py for the `cpu_baseline` field and for `--impl reference`.
+//
+//   ref_bench <bench> <variants.txt> <n_tests> <test_seed> <threads> <max_seconds>
+//             [budget=1000000] [tolerance=0]
+//
+// variants.txt: one patch per line as compact JSON (patch_to_json format).
+// Prints one JSON object: variants, executions (tests actually run, i.e. up to
+// and including the first failing one), ir (reference dynamic instruction
+// count of those executions), seconds, threads.
+
+#include "evoir/corpus.hpp"
+#include "evoir/engine.hpp"
+
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <fstream>
+#include <iostream>
+#include <thread>
+
+using namespace evoir;
+
+int main(int argc, char** argv) {
+    if (argc < 7) {
+        std::cerr << "usage: ref_bench <bench> <variants.txt> <n_tests> <test_seed> <threads> "
+                     "<max_seconds> [budget] [tolerance]\n";
+        return 1;
+    }
+    Benchmark b = load_benchmark(argv[1]);
+    std::ifstream in(argv[2]);
+    int n_tests = std::stoi(argv[3]);
+    uint64_t seed = std::stoull(argv[4]);
+    int threads = std::stoi(argv[5]);
+    double max_seconds = std::stod(argv[6]);
+    int64_t budget = argc > 7 ? std::stoll(argv[7]) : 1000000;
+    double tol = argc > 8 ? std::stod(argv[8]) : 0.0;
+
+    std::vector<Kernel> variants;
+    std::string line;
+    while (std::getline(in, line)) {
+        if (line.empty())
+            continue;
+        variants.push_back(apply_patch(b.kernel, patch_from_json(line)).kernel);
+    }
+    auto tests = generate_tests(b, n_tests, seed);
+    ExecConfig cfg = ExecConfig::for_kernel(b.kernel);
+    cfg.instruction_budget = budget;
+    ExecConfig unit = cfg;
+    {
+        CostTable& t = unit.cost_table;
+        t.arith = t.cmp = t.select_op = t.phi = t.constant = t.br = t.intrinsic = t.getindex = 1;
+        t.load_shared = t.store_shared = t.load_global = t.store_global = t.sync = t.ret = 1;
+    }
+
+    std::atomic<size_t> next{0};
+    std::atomic<bool> stop{false};
+    std::vector<char> done(variants.size(), 0);
+    auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&] {
+        return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    };
+    std::vector<std::thread> pool;
+    for (int w = 0; w < threads; ++w)
+        pool.emplace_back([&] {
+            for (;;) {
+                size_t i = next.fetch_add(1);
+                if (i >= variants.size() || stop.load())
+                    return;
+                if (is_valid(variants[i]))
+                    (void)evaluate_fitness(variants[i], tests, cfg, tol);
+                done[i] = 1;
+                if (elapsed() > max_seconds)
+                    stop.store(true);
+            }
+        });
+    for (auto& t : pool)
+        t.join();
+    double secs = elapsed();
+
+    // Counting pass (untimed): executions and dynamic IR of the same work.
+    int64_t execs = 0, ir = 0, processed = 0;
+    for (size_t i = 0; i < variants.size(); ++i) {
+        if (!done[i])
+            continue;
+        ++processed;
+        if (!is_valid(variants[i]))
+            continue;
+        for (const auto& t : tests) {
+            ExecResult r = execute(variants[i], t, unit);
+            ++execs;
+            ir += r.cost;
+            if (r.status != ExecStatus::Completed)
+                break;
+            if (compute_error(r.outputs, t.oracle) > tol)
+                break;
+        }
+    }
+    std::printf("{\"variants\": %lld, \"executions\": %lld, \"ir\": %lld, \"seconds\": %.6f, "
+                "\"threads\": %d}\n",
+                static_cast<long long>(processed), static_cast<long long>(execs),
+                static_cast<long long>(ir), secs, threads);
+    return 0;
+}

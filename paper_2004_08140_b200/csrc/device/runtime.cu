@@ -1,0 +1,568 @@
+// Device runtime: memory, uploads, launches and read-back for the batched
+// interpreter and the GPU ranking. Called from the C++ host (engine, evoir::
+// wrappers) and the C ABI.
+#include "../host/runtime.hpp"
+#include "interp.cuh"
+#include "nsga_rank.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+namespace evoir::b200 {
+
+namespace {
+
+void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+// Growable device allocation.
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    void reserve(size_t bytes) {
+        if (bytes <= cap)
+            return;
+        if (ptr)
+            cudaFree(ptr);
+        ptr = nullptr;
+        const size_t want = std::max<size_t>(bytes, cap * 3 / 2);
+        check(cudaMalloc(&ptr, want), "cudaMalloc");
+        cap = want;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(ptr); }
+    ~DevBuf() {
+        if (ptr)
+            cudaFree(ptr);
+    }
+};
+
+// Growable pinned host staging buffer.
+struct PinnedBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    void reserve(size_t bytes) {
+        if (bytes <= cap)
+            return;
+        if (ptr)
+            cudaFreeHost(ptr);
+        const size_t want = std::max<size_t>(bytes, cap * 3 / 2);
+        check(cudaMallocHost(&ptr, want), "cudaMallocHost");
+        cap = want;
+    }
+    ~PinnedBuf() {
+        if (ptr)
+            cudaFreeHost(ptr);
+    }
+};
+
+} // namespace
+
+struct DeviceImpl {
+    int ordinal = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+    DevBuf blob, rec, vrec, first_fail, priv, sh_tag, sh_val;
+    DevBuf ts_pos, ts_prev, ts_exec, ts_stop, ts_val, ts_tag;
+    DevBuf rank;
+    PinnedBuf h_blob, h_vrec, h_rec;
+    size_t scratch_budget = size_t(8) << 30; // bytes of per-instance scratch per launch
+};
+
+struct SuiteImpl {
+    DevBuf param_tag, param_payload, buf_size, buf_elem, setup_code, setup_aux, pool, entry_begin,
+        entries, static_err;
+};
+
+Device::Device(int ordinal) : impl_(std::make_unique<DeviceImpl>()) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        throw DeviceUnavailable("no CUDA device available: the B200 interpreter has no CPU path");
+    }
+    if (ordinal < 0) {
+        const char* env = std::getenv("GEVO_DEVICE");
+        if (env)
+            ordinal = std::atoi(env);
+        else
+            check(cudaGetDevice(&ordinal), "cudaGetDevice");
+    }
+    impl_->ordinal = ordinal;
+    check(cudaSetDevice(ordinal), "cudaSetDevice");
+    check(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    check(cudaEventCreate(&impl_->ev0), "cudaEventCreate");
+    check(cudaEventCreate(&impl_->ev1), "cudaEventCreate");
+    check(cudaEventCreate(&impl_->ev2), "cudaEventCreate");
+}
+
+Device::~Device() {
+    if (impl_->stream)
+        cudaStreamDestroy(impl_->stream);
+    cudaEventDestroy(impl_->ev0);
+    cudaEventDestroy(impl_->ev1);
+    cudaEventDestroy(impl_->ev2);
+}
+
+int Device::ordinal() const { return impl_->ordinal; }
+
+Device& Device::default_device() {
+    static Device* dev = new Device(-1); // intentionally leaked: outlives static teardown
+    return *dev;
+}
+
+namespace {
+
+template <typename T>
+void upload(DevBuf& b, const std::vector<T>& v, cudaStream_t s) {
+    b.reserve(std::max<size_t>(v.size() * sizeof(T), 16));
+    if (!v.empty())
+        check(cudaMemcpyAsync(b.ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s),
+              "upload");
+}
+
+} // namespace
+
+DeviceSuite::DeviceSuite(Device& dev, SuiteImage image)
+    : dev_(dev), image_(std::move(image)), impl_(std::make_unique<SuiteImpl>()) {
+    std::lock_guard<std::mutex> g(dev_.lock());
+    check(cudaSetDevice(dev_.ordinal()), "cudaSetDevice");
+    cudaStream_t s = dev_.impl().stream;
+    SuiteImpl& d = *impl_;
+    upload(d.param_tag, image_.param_tag, s);
+    upload(d.param_payload, image_.param_payload, s);
+    upload(d.buf_size, image_.buf_size, s);
+    upload(d.buf_elem, image_.buf_elem, s);
+    upload(d.setup_code, image_.setup_code, s);
+    upload(d.setup_aux, image_.setup_aux, s);
+    upload(d.pool, image_.pool, s);
+    upload(d.entry_begin, image_.entry_begin, s);
+    std::vector<gevo::OracleEntryDev> ents;
+    for (const auto& e : image_.entries)
+        ents.push_back(gevo::OracleEntryDev{e.param, e.size, e.off, e.elem, 0});
+    upload(d.entries, ents, s);
+    upload(d.static_err, image_.static_err, s);
+    check(cudaStreamSynchronize(s), "suite upload");
+}
+
+DeviceSuite::~DeviceSuite() = default;
+
+namespace {
+
+// Scratch bytes one instance needs in a launch.
+size_t scratch_per_instance(const SuiteImage& S, uint64_t writable_any, const ExecImage& ex,
+                            bool any_sync, uint32_t max_values) {
+    size_t b = 0;
+    for (int p = 0; p < S.n_params; ++p)
+        if ((writable_any >> p) & 1ull)
+            b += 4 * static_cast<size_t>(S.pool_rows[static_cast<size_t>(p)]);
+    b += 5 * static_cast<size_t>(std::max(ex.shared_words, 0));
+    if (any_sync)
+        b += static_cast<size_t>(ex.threads) * (4 + 4 + 8 + 4 + 5 * static_cast<size_t>(max_values));
+    return b;
+}
+
+struct Launch {
+    gevo::InterpArgs A;
+    size_t chunk;
+};
+
+// Fills everything but the batch pointers and the per-chunk window.
+gevo::InterpArgs base_args(DeviceSuite& suite, const ExecImage& ex, const EvalOptions& opt) {
+    gevo::InterpArgs A{};
+    const SuiteImage& S = suite.image();
+    SuiteImpl& d = suite.impl();
+    A.n_tests = S.n_tests;
+    A.n_params = S.n_params;
+    A.param_tag = d.param_tag.as<uint8_t>();
+    A.param_payload = d.param_payload.as<uint32_t>();
+    A.buf_size = d.buf_size.as<int32_t>();
+    A.buf_elem = d.buf_elem.as<uint8_t>();
+    A.setup_code = d.setup_code.as<uint8_t>();
+    A.setup_aux = d.setup_aux.as<int32_t>();
+    A.pool = d.pool.as<uint32_t>();
+    A.entry_begin = d.entry_begin.as<int32_t>();
+    A.entries = d.entries.as<gevo::OracleEntryDev>();
+    A.static_err = d.static_err.as<uint8_t>();
+    for (int p = 0; p < S.n_params; ++p)
+        A.pool_off[p] = S.pool_off[static_cast<size_t>(p)];
+    A.threads = ex.threads;
+    A.shared_words = ex.shared_words;
+    A.budget = ex.budget;
+    for (int c = 0; c < GEVO_COST_CLASSES; ++c)
+        A.cost[c] = ex.cost[static_cast<size_t>(c)];
+    A.tolerance = opt.tolerance;
+    A.early_exit = opt.early_exit ? 1 : 0;
+    return A;
+}
+
+void bind_batch(gevo::InterpArgs& A, const void* dblob, const gevo_batch_header& h) {
+    const char* base = static_cast<const char*>(dblob);
+    A.variants = reinterpret_cast<const gevo_variant*>(base + h.off_variants);
+    A.blocks = reinterpret_cast<const gevo_block*>(base + h.off_blocks);
+    A.insts = reinterpret_cast<const gevo_inst*>(base + h.off_insts);
+    A.arms = reinterpret_cast<const gevo_arm*>(base + h.off_arms);
+    A.lit_payload = reinterpret_cast<const uint32_t*>(base + h.off_lit_payload);
+    A.lit_tag = reinterpret_cast<const uint8_t*>(base + h.off_lit_tag);
+    A.n_variants = h.n_variants;
+    A.max_slots = std::max<uint32_t>(h.max_slots, 1);
+    A.ts_slots = std::max<uint32_t>(h.max_values, 1);
+}
+
+// Launches the interpreter over all instances in scratch-bounded chunks, then
+// the per-variant reduction. Records land in dev.rec / dev.vrec.
+int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const gevo_batch_header& h,
+               uint64_t writable_any, const ExecImage& ex, const EvalOptions& opt,
+               cudaStream_t s) {
+    const SuiteImage& S = suite.image();
+    if (h.max_slots > gevo::kMaxSlots32)
+        throw std::invalid_argument("variant value file exceeds the device limit");
+    const uint64_t total = static_cast<uint64_t>(h.n_variants) * static_cast<uint64_t>(S.n_tests);
+    dev.rec.reserve(std::max<size_t>(total * sizeof(gevo_test_record), 16));
+    dev.vrec.reserve(std::max<size_t>(h.n_variants * sizeof(gevo_variant_record), 16));
+    dev.first_fail.reserve(std::max<size_t>(h.n_variants * sizeof(int32_t), 16));
+    if (opt.early_exit)
+        check(cudaMemsetAsync(dev.first_fail.ptr, 0x7f, h.n_variants * sizeof(int32_t), s),
+              "memset first_fail");
+    A.rec = dev.rec.as<gevo_test_record>();
+    A.first_fail = dev.first_fail.as<int32_t>();
+
+    const size_t per = std::max<size_t>(
+        scratch_per_instance(S, writable_any, ex, h.any_sync != 0, h.max_values), 1);
+    size_t chunk = std::min<uint64_t>(total, std::max<size_t>(dev.scratch_budget / per, 128));
+    chunk = std::min<size_t>(chunk, size_t(1) << 30);
+    int launches = 0;
+    // scratch layout for a chunk
+    size_t priv_words = 0;
+    for (int p = 0; p < S.n_params; ++p) {
+        A.priv_off[p] = priv_words * chunk;
+        if ((writable_any >> p) & 1ull)
+            priv_words += static_cast<size_t>(S.pool_rows[static_cast<size_t>(p)]);
+    }
+    dev.priv.reserve(std::max<size_t>(priv_words * chunk * 4, 16));
+    const size_t sw = static_cast<size_t>(std::max(ex.shared_words, 0));
+    dev.sh_tag.reserve(std::max<size_t>(sw * chunk, 16));
+    dev.sh_val.reserve(std::max<size_t>(sw * chunk * 4, 16));
+    A.priv = dev.priv.as<uint32_t>();
+    A.sh_tag = dev.sh_tag.as<uint8_t>();
+    A.sh_val = dev.sh_val.as<uint32_t>();
+    if (h.any_sync) {
+        const size_t tn = static_cast<size_t>(ex.threads) * chunk;
+        dev.ts_pos.reserve(tn * 4);
+        dev.ts_prev.reserve(tn * 4);
+        dev.ts_exec.reserve(tn * 8);
+        dev.ts_stop.reserve(tn * 4);
+        dev.ts_val.reserve(tn * A.ts_slots * 4);
+        dev.ts_tag.reserve(tn * A.ts_slots);
+        A.ts_pos = dev.ts_pos.as<int32_t>();
+        A.ts_prev = dev.ts_prev.as<int32_t>();
+        A.ts_exec = dev.ts_exec.as<int64_t>();
+        A.ts_stop = dev.ts_stop.as<uint32_t>();
+        A.ts_val = dev.ts_val.as<uint32_t>();
+        A.ts_tag = dev.ts_tag.as<uint8_t>();
+    }
+    for (uint64_t begin = 0; begin < total; begin += chunk) {
+        A.inst_begin = begin;
+        A.n_inst = static_cast<uint32_t>(std::min<uint64_t>(chunk, total - begin));
+        // priv_off is laid out for `chunk` rows; the last chunk may be shorter,
+        // so keep the stride equal to the chunk capacity.
+        gevo::InterpArgs L = A;
+        L.n_inst = A.n_inst;
+        if (L.n_inst != chunk) {
+            // Re-lay out the private regions for the shorter window.
+            size_t words = 0;
+            for (int p = 0; p < S.n_params; ++p) {
+                L.priv_off[p] = words * L.n_inst;
+                if ((writable_any >> p) & 1ull)
+                    words += static_cast<size_t>(S.pool_rows[static_cast<size_t>(p)]);
+            }
+        }
+        check(gevo::launch_interp(L, s), "interp_kernel launch");
+        ++launches;
+    }
+    check(gevo::launch_fitness(dev.rec.as<gevo_test_record>(), h.n_variants, S.n_tests,
+                               opt.tolerance, dev.vrec.as<gevo_variant_record>(), s),
+          "fitness_kernel launch");
+    return launches + 1;
+}
+
+uint64_t writable_union(BatchImage& batch) {
+    const auto& blob = batch.blob();
+    const auto& h = batch.header();
+    uint64_t m = 0;
+    const auto* vars = reinterpret_cast<const gevo_variant*>(blob.data() + h.off_variants);
+    for (uint32_t v = 0; v < h.n_variants; ++v)
+        m |= vars[v].writable;
+    return m;
+}
+
+} // namespace
+
+EvalResult evaluate(DeviceSuite& suite, BatchImage& batch, const ExecImage& exec,
+                    const EvalOptions& opt) {
+    Device& devh = suite.device();
+    std::lock_guard<std::mutex> g(devh.lock());
+    DeviceImpl& dev = devh.impl();
+    check(cudaSetDevice(dev.ordinal), "cudaSetDevice");
+    cudaStream_t s = dev.stream;
+    const SuiteImage& S = suite.image();
+    EvalResult R;
+    const std::vector<uint8_t>& blob = batch.blob();
+    const gevo_batch_header h = batch.header();
+    const uint64_t wr = writable_union(batch);
+
+    dev.h_blob.reserve(blob.size());
+    std::memcpy(dev.h_blob.ptr, blob.data(), blob.size());
+    dev.blob.reserve(blob.size());
+    check(cudaEventRecord(dev.ev0, s), "event");
+    check(cudaMemcpyAsync(dev.blob.ptr, dev.h_blob.ptr, blob.size(), cudaMemcpyHostToDevice, s),
+          "blob H2D");
+    R.h2d_bytes = blob.size();
+    gevo::InterpArgs A = base_args(suite, exec, opt);
+    bind_batch(A, dev.blob.ptr, h);
+    check(cudaEventRecord(dev.ev1, s), "event");
+    R.launches = launch_all(dev, suite, A, h, wr, exec, opt, s);
+    check(cudaEventRecord(dev.ev2, s), "event");
+
+    R.variants.resize(h.n_variants);
+    if (h.n_variants) {
+        check(cudaMemcpyAsync(R.variants.data(), dev.vrec.ptr,
+                              h.n_variants * sizeof(gevo_variant_record), cudaMemcpyDeviceToHost, s),
+              "records D2H");
+        R.d2h_bytes += h.n_variants * sizeof(gevo_variant_record);
+    }
+    const size_t total = static_cast<size_t>(h.n_variants) * S.n_tests;
+    if (opt.want_tests || opt.want_outputs) {
+        R.tests.resize(total);
+        if (total)
+            check(cudaMemcpyAsync(R.tests.data(), dev.rec.ptr, total * sizeof(gevo_test_record),
+                                  cudaMemcpyDeviceToHost, s),
+                  "test records D2H");
+        R.d2h_bytes += total * sizeof(gevo_test_record);
+    }
+    std::vector<uint32_t> priv;
+    size_t chunk = total;
+    if (opt.want_outputs && total) {
+        // Only supported when every instance ran in one launch window.
+        if (R.launches != 2)
+            throw std::invalid_argument("want_outputs needs a single-launch batch");
+        size_t words = 0;
+        for (int p = 0; p < S.n_params; ++p)
+            if ((wr >> p) & 1ull)
+                words += static_cast<size_t>(S.pool_rows[static_cast<size_t>(p)]);
+        priv.resize(words * chunk);
+        if (!priv.empty())
+            check(cudaMemcpyAsync(priv.data(), dev.priv.ptr, priv.size() * 4,
+                                  cudaMemcpyDeviceToHost, s),
+                  "outputs D2H");
+    }
+    check(cudaStreamSynchronize(s), "evaluate");
+    float ms = 0.0f;
+    check(cudaEventElapsedTime(&ms, dev.ev1, dev.ev2), "elapsed");
+    R.kernel_ms = ms;
+
+    if (opt.want_outputs && total) {
+        const auto* vars = reinterpret_cast<const gevo_variant*>(blob.data() + h.off_variants);
+        R.outputs.assign(h.n_variants, std::vector<BufferMap>(static_cast<size_t>(S.n_tests)));
+        for (uint32_t v = 0; v < h.n_variants; ++v)
+            for (int t = 0; t < S.n_tests; ++t) {
+                const size_t gi = static_cast<size_t>(v) * S.n_tests + t;
+                if (R.tests[gi].status != GEVO_STATUS_COMPLETED)
+                    continue;
+                BufferMap& out = R.outputs[v][static_cast<size_t>(t)];
+                size_t off_words = 0;
+                for (int p = 0; p < S.n_params; ++p) {
+                    const Param& prm = S.params[static_cast<size_t>(p)];
+                    const bool global = prm.type.is_ptr() && prm.type.space == MemSpace::Global;
+                    const bool w = (wr >> p) & 1ull;
+                    const size_t region = off_words * chunk;
+                    if (w)
+                        off_words += static_cast<size_t>(S.pool_rows[static_cast<size_t>(p)]);
+                    if (!global)
+                        continue;
+                    const size_t tp = static_cast<size_t>(t) * S.n_params + p;
+                    const int32_t n = S.buf_size[tp];
+                    Buffer b;
+                    b.elem = S.buf_elem[tp] == GEVO_TAG_I32 ? TypeKind::I32 : TypeKind::F32;
+                    const bool mine = (vars[v].writable >> p) & 1ull;
+                    for (int32_t e = 0; e < n; ++e) {
+                        const uint32_t word =
+                            mine ? priv[region + static_cast<size_t>(e) * chunk + gi]
+                                 : S.pool[S.pool_off[static_cast<size_t>(p)] +
+                                          static_cast<size_t>(e) * S.n_tests + t];
+                        if (b.elem == TypeKind::I32) {
+                            int32_t x;
+                            std::memcpy(&x, &word, 4);
+                            b.i.push_back(x);
+                        } else {
+                            float x;
+                            std::memcpy(&x, &word, 4);
+                            b.f.push_back(x);
+                        }
+                    }
+                    out[prm.name] = std::move(b);
+                }
+            }
+    }
+    return R;
+}
+
+struct ResidentBatch {
+    DeviceSuite* suite;
+    DevBuf blob;
+    gevo_batch_header h;
+    uint64_t writable;
+};
+
+std::shared_ptr<ResidentBatch> make_resident(DeviceSuite& suite, BatchImage& batch) {
+    Device& devh = suite.device();
+    std::lock_guard<std::mutex> g(devh.lock());
+    check(cudaSetDevice(devh.ordinal()), "cudaSetDevice");
+    auto rb = std::make_shared<ResidentBatch>();
+    rb->suite = &suite;
+    const auto& blob = batch.blob();
+    rb->h = batch.header();
+    rb->writable = writable_union(batch);
+    rb->blob.reserve(blob.size());
+    check(cudaMemcpy(rb->blob.ptr, blob.data(), blob.size(), cudaMemcpyHostToDevice), "resident");
+    return rb;
+}
+
+float evaluate_resident(ResidentBatch& rb, const ExecImage& exec, const EvalOptions& opt,
+                        float* interp_ms, std::vector<gevo_variant_record>* out) {
+    Device& devh = rb.suite->device();
+    std::lock_guard<std::mutex> g(devh.lock());
+    DeviceImpl& dev = devh.impl();
+    check(cudaSetDevice(dev.ordinal), "cudaSetDevice");
+    cudaStream_t s = dev.stream;
+    gevo::InterpArgs A = base_args(*rb.suite, exec, opt);
+    bind_batch(A, rb.blob.ptr, rb.h);
+    check(cudaEventRecord(dev.ev0, s), "event");
+    launch_all(dev, *rb.suite, A, rb.h, rb.writable, exec, opt, s);
+    check(cudaEventRecord(dev.ev2, s), "event");
+    if (out) {
+        out->resize(rb.h.n_variants);
+        check(cudaMemcpyAsync(out->data(), dev.vrec.ptr, rb.h.n_variants * sizeof(gevo_variant_record),
+                              cudaMemcpyDeviceToHost, s),
+              "records");
+    }
+    check(cudaStreamSynchronize(s), "resident eval");
+    float ms = 0;
+    check(cudaEventElapsedTime(&ms, dev.ev0, dev.ev2), "elapsed");
+    if (interp_ms)
+        *interp_ms = ms;
+    return ms;
+}
+
+ParetoRank rank_on_device(Device& devh, const std::vector<FitnessVector>& fits, bool single_group) {
+    ParetoRank r;
+    const int32_t n = static_cast<int32_t>(fits.size());
+    r.front.assign(fits.size(), -1);
+    r.crowding.assign(fits.size(), 0.0);
+    if (n == 0)
+        return r;
+    std::lock_guard<std::mutex> g(devh.lock());
+    DeviceImpl& dev = devh.impl();
+    check(cudaSetDevice(dev.ordinal), "cudaSetDevice");
+    cudaStream_t s = dev.stream;
+    const size_t N = static_cast<size_t>(n);
+    // layout: cost, err, stair, crowd (double); order, front, offsets(n+1), fill, members,
+    // ord_cost, ord_err, n_fronts (int32)
+    const size_t dbytes = 4 * N * 8, ibytes = (7 * N + 2) * 4;
+    dev.rank.reserve(dbytes + ibytes);
+    char* base = dev.rank.as<char>();
+    gevo::RankBuffers B{};
+    double* dcost = reinterpret_cast<double*>(base);
+    double* derr = dcost + N;
+    B.cost = dcost;
+    B.err = derr;
+    B.stair = derr + N;
+    B.crowd = derr + 2 * N;
+    int32_t* ib = reinterpret_cast<int32_t*>(base + dbytes);
+    B.order = ib;
+    B.front = ib + N;
+    B.offsets = ib + 2 * N;
+    B.fill = ib + 3 * N + 1;
+    B.members = ib + 4 * N + 1;
+    B.ord_cost = ib + 5 * N + 1;
+    B.ord_err = ib + 6 * N + 1;
+    B.n_fronts = ib + 7 * N + 1;
+    std::vector<double> hc(N), he(N);
+    for (size_t i = 0; i < N; ++i) {
+        hc[i] = fits[i].cost;
+        he[i] = fits[i].error;
+    }
+    check(cudaMemcpyAsync(dcost, hc.data(), N * 8, cudaMemcpyHostToDevice, s), "rank H2D");
+    check(cudaMemcpyAsync(derr, he.data(), N * 8, cudaMemcpyHostToDevice, s), "rank H2D");
+    check(gevo::launch_rank(B, n, single_group, s), "rank kernels");
+    std::vector<int32_t> front(N), members(N), offsets(N + 1);
+    int32_t F = 0;
+    check(cudaMemcpyAsync(front.data(), B.front, N * 4, cudaMemcpyDeviceToHost, s), "rank D2H");
+    check(cudaMemcpyAsync(members.data(), B.members, N * 4, cudaMemcpyDeviceToHost, s), "rank D2H");
+    check(cudaMemcpyAsync(offsets.data(), B.offsets, (N + 1) * 4, cudaMemcpyDeviceToHost, s),
+          "rank D2H");
+    check(cudaMemcpyAsync(r.crowding.data(), B.crowd, N * 8, cudaMemcpyDeviceToHost, s), "rank D2H");
+    check(cudaMemcpyAsync(&F, B.n_fronts, 4, cudaMemcpyDeviceToHost, s), "rank D2H");
+    check(cudaStreamSynchronize(s), "rank");
+    for (size_t i = 0; i < N; ++i)
+        r.front[i] = front[i];
+    r.fronts.resize(static_cast<size_t>(F));
+    for (int32_t f = 0; f < F; ++f)
+        r.fronts[static_cast<size_t>(f)].assign(members.begin() + offsets[static_cast<size_t>(f)],
+                                                members.begin() + offsets[static_cast<size_t>(f) + 1]);
+    return r;
+}
+
+double error_on_device(Device& devh, const BufferMap& candidate, const BufferMap& oracle) {
+    // Structural mismatches are decided on the host exactly like the suite
+    // builder; the element-wise metric runs on the device.
+    std::vector<uint32_t> cw, ow;
+    std::vector<uint8_t> el;
+    for (const auto& [name, want] : oracle) {
+        const auto it = candidate.find(name);
+        if (it == candidate.end() || it->second.elem != want.elem || it->second.size() != want.size())
+            return 1.0;
+        for (size_t e = 0; e < want.size(); ++e) {
+            uint32_t c, o;
+            if (want.elem == TypeKind::I32) {
+                std::memcpy(&c, &it->second.i[e], 4);
+                std::memcpy(&o, &want.i[e], 4);
+            } else {
+                std::memcpy(&c, &it->second.f[e], 4);
+                std::memcpy(&o, &want.f[e], 4);
+            }
+            cw.push_back(c);
+            ow.push_back(o);
+            el.push_back(want.elem == TypeKind::I32 ? GEVO_TAG_I32 : GEVO_TAG_F32);
+        }
+    }
+    if (cw.empty())
+        return 0.0;
+    std::lock_guard<std::mutex> g(devh.lock());
+    DeviceImpl& dev = devh.impl();
+    check(cudaSetDevice(dev.ordinal), "cudaSetDevice");
+    cudaStream_t s = dev.stream;
+    const size_t n = cw.size();
+    dev.rank.reserve(n * 9 + 64);
+    char* base = dev.rank.as<char>();
+    uint32_t* dc = reinterpret_cast<uint32_t*>(base);
+    uint32_t* dor = dc + n;
+    double* dres = reinterpret_cast<double*>(base + ((8 * n + 15) & ~size_t(15)));
+    uint8_t* de = reinterpret_cast<uint8_t*>(dres + 1);
+    check(cudaMemcpyAsync(dc, cw.data(), n * 4, cudaMemcpyHostToDevice, s), "err H2D");
+    check(cudaMemcpyAsync(dor, ow.data(), n * 4, cudaMemcpyHostToDevice, s), "err H2D");
+    check(cudaMemcpyAsync(de, el.data(), n, cudaMemcpyHostToDevice, s), "err H2D");
+    check(gevo::launch_error(dc, dor, de, static_cast<uint32_t>(n), dres, s), "error kernel");
+    double res = 0.0;
+    check(cudaMemcpyAsync(&res, dres, 8, cudaMemcpyDeviceToHost, s), "err D2H");
+    check(cudaStreamSynchronize(s), "error");
+    return res;
+}
+
+} // namespace evoir::b200

@@ -1,0 +1,528 @@
+// Variant encoder and test-suite layout for the sm_100a interpreter.
+//
+// Everything Machine's constructor and compile() resolve per execution in the
+// reference (src/vm.cpp:83-112 parameter binding and setup traps, 166-193
+// label -> block, cost by static pointer space, value slots) is resolved here
+// once per variant / per suite, so the device loop only decodes integers.
+#include "encode.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <unordered_map>
+
+namespace evoir::b200 {
+
+namespace {
+
+uint8_t scalar_tag(TypeKind k) {
+    switch (k) {
+    case TypeKind::I32: return GEVO_TAG_I32;
+    case TypeKind::F32: return GEVO_TAG_F32;
+    case TypeKind::Bool: return GEVO_TAG_BOOL;
+    default: return GEVO_TAG_NEVER;
+    }
+}
+
+uint32_t scalar_bits(const Scalar& s) {
+    uint32_t w = 0;
+    if (s.kind == TypeKind::I32)
+        std::memcpy(&w, &s.i, 4);
+    else if (s.kind == TypeKind::F32)
+        std::memcpy(&w, &s.f, 4);
+    else
+        w = s.b ? 1u : 0u;
+    return w;
+}
+
+uint32_t buffer_word(const Buffer& b, size_t e) {
+    uint32_t w;
+    if (b.elem == TypeKind::I32)
+        std::memcpy(&w, &b.i[e], 4);
+    else
+        std::memcpy(&w, &b.f[e], 4);
+    return w;
+}
+
+bool is_global_ptr(const Param& p) { return p.type.is_ptr() && p.type.space == MemSpace::Global; }
+
+uint8_t cost_class(const Kernel& k, const Instruction& in) {
+    switch (in.op) {
+    case Opcode::Add: case Opcode::Sub: case Opcode::Mul: case Opcode::SDiv:
+    case Opcode::FAdd: case Opcode::FSub: case Opcode::FMul: case Opcode::FDiv:
+        return GEVO_COST_ARITH;
+    case Opcode::ICmp: case Opcode::FCmp: return GEVO_COST_CMP;
+    case Opcode::Select: return GEVO_COST_SELECT;
+    case Opcode::Phi: return GEVO_COST_PHI;
+    case Opcode::Const: return GEVO_COST_CONST;
+    case Opcode::Br: return GEVO_COST_BR;
+    case Opcode::Tid: case Opcode::NThreads: return GEVO_COST_INTRINSIC;
+    case Opcode::GetIndex: return GEVO_COST_GETINDEX;
+    case Opcode::Sync: return GEVO_COST_SYNC;
+    case Opcode::Ret: return GEVO_COST_RET;
+    case Opcode::Load: case Opcode::Store: {
+        // Space from the pointer operand's static type; Global when unresolved.
+        bool shared = false;
+        if (!in.operands.empty()) {
+            const auto t = operand_type(k, in.operands[0]);
+            shared = t && t->is_ptr() && t->space == MemSpace::Shared;
+        }
+        if (in.op == Opcode::Load)
+            return shared ? GEVO_COST_LOAD_SHARED : GEVO_COST_LOAD_GLOBAL;
+        return shared ? GEVO_COST_STORE_SHARED : GEVO_COST_STORE_GLOBAL;
+    }
+    }
+    return GEVO_COST_ARITH;
+}
+
+} // namespace
+
+ExecImage exec_image(const ExecConfig& cfg) {
+    ExecImage e;
+    e.threads = cfg.thread_count;
+    e.shared_words = cfg.shared_words;
+    e.budget = cfg.instruction_budget;
+    const CostTable& c = cfg.cost_table;
+    e.cost = {c.arith,       c.cmp,          c.select_op,   c.phi,          c.constant,
+              c.br,          c.intrinsic,    c.getindex,    c.load_shared,  c.store_shared,
+              c.load_global, c.store_global, c.sync,        c.ret};
+    return e;
+}
+
+SuiteImage build_suite(const std::vector<Param>& params, const std::vector<TestCase>& tests) {
+    if (params.size() > GEVO_MAX_PARAMS)
+        throw std::invalid_argument("kernel has more than 48 parameters");
+    SuiteImage s;
+    s.params = params;
+    s.n_tests = static_cast<int>(tests.size());
+    s.n_params = static_cast<int>(params.size());
+    const size_t T = tests.size(), P = params.size();
+    for (const Param& p : params)
+        s.param_names.push_back(p.name);
+    s.param_tag.assign(T * P, GEVO_TAG_UNDEF);
+    s.param_payload.assign(T * P, 0);
+    s.buf_size.assign(T * P, 0);
+    s.buf_elem.assign(T * P, GEVO_TAG_NEVER);
+    s.setup_code.assign(T, GEVO_OK);
+    s.setup_aux.assign(T, -1);
+    s.static_err.assign(T, 0);
+
+    // Parameter binding, first failing parameter wins (src/vm.cpp:86-110).
+    for (size_t t = 0; t < T; ++t) {
+        for (size_t p = 0; p < P; ++p) {
+            const Param& prm = params[p];
+            const size_t tp = t * P + p;
+            auto fail = [&](uint8_t code) {
+                if (s.setup_code[t] == GEVO_OK) {
+                    s.setup_code[t] = code;
+                    s.setup_aux[t] = static_cast<int32_t>(p);
+                }
+            };
+            if (prm.type.is_ptr()) {
+                if (prm.type.space == MemSpace::Shared) {
+                    s.param_tag[tp] = GEVO_TAG_PTR_SHARED;
+                    continue;
+                }
+                const auto it = tests[t].inputs.find(prm.name);
+                if (it == tests[t].inputs.end()) {
+                    fail(GEVO_TRAP_MISSING_BUFFER);
+                    continue;
+                }
+                if (prm.elem && *prm.elem != it->second.elem) {
+                    fail(GEVO_TRAP_BUFFER_TYPE);
+                    continue;
+                }
+                s.param_tag[tp] = static_cast<uint8_t>(GEVO_TAG_PTR_GLOBAL | p);
+                s.buf_size[tp] = static_cast<int32_t>(it->second.size());
+                s.buf_elem[tp] = scalar_tag(it->second.elem);
+            } else {
+                const auto it = tests[t].scalars.find(prm.name);
+                if (it == tests[t].scalars.end()) {
+                    fail(GEVO_TRAP_MISSING_SCALAR);
+                    continue;
+                }
+                if (it->second.type() != prm.type) {
+                    fail(GEVO_TRAP_SCALAR_TYPE);
+                    continue;
+                }
+                s.param_tag[tp] = scalar_tag(it->second.kind);
+                s.param_payload[tp] = scalar_bits(it->second);
+            }
+        }
+    }
+
+    // Inputs: one [rows][T] block per global parameter.
+    s.pool_off.assign(P, 0);
+    s.pool_rows.assign(P, 0);
+    for (size_t p = 0; p < P; ++p) {
+        if (!is_global_ptr(params[p]))
+            continue;
+        int32_t rows = 0;
+        for (size_t t = 0; t < T; ++t)
+            rows = std::max(rows, s.buf_size[t * P + p]);
+        s.pool_rows[p] = rows;
+        s.pool_off[p] = s.pool.size();
+        s.pool.resize(s.pool.size() + static_cast<size_t>(rows) * T, 0u);
+        for (size_t t = 0; t < T; ++t) {
+            if (s.param_tag[t * P + p] == GEVO_TAG_UNDEF)
+                continue;
+            const Buffer& b = tests[t].inputs.at(params[p].name);
+            for (size_t e = 0; e < b.size(); ++e)
+                s.pool[s.pool_off[p] + e * T + t] = buffer_word(b, e);
+        }
+    }
+
+    // Oracles (compute_error, src/vm.cpp:536-556): outputs are all global
+    // parameters by name, the last parameter of a name winning the map slot.
+    std::unordered_map<std::string, int> out_param;
+    for (size_t p = 0; p < P; ++p)
+        if (is_global_ptr(params[p]))
+            out_param[params[p].name] = static_cast<int>(p);
+    std::map<std::string, std::pair<uint64_t, int32_t>> region; // name -> (off, rows)
+    for (size_t t = 0; t < T; ++t)
+        for (const auto& [name, ob] : tests[t].oracle) {
+            auto& r = region[name];
+            r.second = std::max(r.second, static_cast<int32_t>(ob.size()));
+        }
+    for (auto& [name, r] : region) {
+        r.first = s.pool.size();
+        s.pool.resize(s.pool.size() + static_cast<size_t>(r.second) * T, 0u);
+    }
+    s.entry_begin.push_back(0);
+    for (size_t t = 0; t < T; ++t) {
+        for (const auto& [name, ob] : tests[t].oracle) {
+            const auto it = out_param.find(name);
+            if (it == out_param.end()) {
+                s.static_err[t] = 1;
+                continue;
+            }
+            const size_t tp = t * P + static_cast<size_t>(it->second);
+            if (s.param_tag[tp] == GEVO_TAG_UNDEF || s.buf_elem[tp] != scalar_tag(ob.elem) ||
+                static_cast<size_t>(s.buf_size[tp]) != ob.size()) {
+                s.static_err[t] = 1;
+                continue;
+            }
+            const auto& r = region.at(name);
+            for (size_t e = 0; e < ob.size(); ++e)
+                s.pool[r.first + e * T + t] = buffer_word(ob, e);
+            s.entries.push_back(SuiteImage::OracleEntry{it->second, static_cast<int32_t>(ob.size()),
+                                                        r.first, scalar_tag(ob.elem)});
+        }
+        s.entry_begin.push_back(static_cast<int32_t>(s.entries.size()));
+    }
+    return s;
+}
+
+BatchImage::BatchImage(const SuiteImage& suite) : suite_(suite) {}
+
+void BatchImage::add(const Kernel& k) {
+    if (!(k.params == suite_.params))
+        throw std::invalid_argument("variant '" + k.name +
+                                    "' does not share the suite's parameter list");
+    if (k.blocks.size() > 32767)
+        throw std::invalid_argument("too many blocks");
+    const uint32_t P = static_cast<uint32_t>(suite_.n_params);
+
+    // Dense value slots in order of first appearance.
+    std::unordered_map<int32_t, uint32_t> slot_of;
+    std::vector<int32_t> slot_ids;
+    auto note = [&](int32_t id) {
+        if (slot_of.emplace(id, static_cast<uint32_t>(slot_ids.size())).second)
+            slot_ids.push_back(id);
+    };
+    k.for_each_instruction([&](const BasicBlock&, const Instruction& in) {
+        if (in.result && *in.result >= 0)
+            note(*in.result);
+        for (const Operand& o : in.operands)
+            if (o.is_value())
+                note(o.value);
+    });
+    const uint32_t V = static_cast<uint32_t>(slot_ids.size());
+    const uint32_t poison_param = V + P;   // tag GEVO_TAG_POISON_PARAM at init
+    const uint32_t poison_missing = V + P + 1;
+    const uint32_t lit_begin = V + P + 2;
+
+    gevo_variant var{};
+    var.inst_base = static_cast<uint32_t>(insts_.size());
+    var.block_base = static_cast<uint32_t>(blocks_.size());
+    var.arm_base = static_cast<uint32_t>(arms_.size());
+    var.lit_base = static_cast<uint32_t>(lit_payload_.size());
+    var.n_values = static_cast<uint16_t>(V);
+    var.n_blocks = static_cast<uint16_t>(k.blocks.size());
+
+    std::unordered_map<uint64_t, uint32_t> lit_slot;
+    uint32_t n_lits = 0;
+    auto literal = [&](const Literal& l) -> uint16_t {
+        const uint8_t tag = scalar_tag(l.kind);
+        const uint32_t bits = scalar_bits(l);
+        const uint64_t key = (static_cast<uint64_t>(tag) << 32) | bits;
+        const auto it = lit_slot.find(key);
+        if (it != lit_slot.end())
+            return static_cast<uint16_t>(lit_begin + it->second);
+        lit_slot.emplace(key, n_lits);
+        lit_tag_.push_back(tag);
+        lit_payload_.push_back(bits);
+        return static_cast<uint16_t>(lit_begin + n_lits++);
+    };
+    auto ref = [&](const Instruction& in, size_t i) -> uint16_t {
+        if (i >= in.operands.size())
+            return static_cast<uint16_t>(poison_missing);
+        const Operand& o = in.operands[i];
+        if (o.kind == Operand::Kind::Value)
+            return static_cast<uint16_t>(slot_of.at(o.value));
+        if (o.kind == Operand::Kind::Param)
+            return static_cast<uint16_t>(o.param >= 0 && static_cast<uint32_t>(o.param) < P
+                                             ? V + static_cast<uint32_t>(o.param)
+                                             : poison_param);
+        return literal(o.lit);
+    };
+
+    // Pointer provenance for privatising writable global buffers: pointers
+    // only originate from parameters and flow through getindex and phi.
+    std::unordered_map<int32_t, uint64_t> prov;
+    auto prov_of = [&](const Operand& o) -> uint64_t {
+        if (o.kind == Operand::Kind::Param)
+            return (o.param >= 0 && static_cast<uint32_t>(o.param) < P &&
+                    is_global_ptr(k.params[static_cast<size_t>(o.param)]))
+                       ? (1ull << o.param)
+                       : 0;
+        if (o.kind == Operand::Kind::Value) {
+            const auto it = prov.find(o.value);
+            return it == prov.end() ? 0 : it->second;
+        }
+        return 0;
+    };
+    for (bool grew = true; grew;) {
+        grew = false;
+        k.for_each_instruction([&](const BasicBlock&, const Instruction& in) {
+            if (!in.result || (in.op != Opcode::GetIndex && in.op != Opcode::Phi))
+                return;
+            uint64_t m = 0;
+            if (in.op == Opcode::GetIndex) {
+                if (!in.operands.empty())
+                    m = prov_of(in.operands[0]);
+            } else {
+                for (const Operand& o : in.operands)
+                    m |= prov_of(o);
+            }
+            uint64_t& cur = prov[*in.result];
+            if ((cur | m) != cur) {
+                cur |= m;
+                grew = true;
+            }
+        });
+    }
+    uint64_t writable = 0;
+    k.for_each_instruction([&](const BasicBlock&, const Instruction& in) {
+        if (in.op == Opcode::Store && !in.operands.empty())
+            writable |= prov_of(in.operands[0]);
+    });
+    var.writable = writable;
+
+    std::unordered_map<int, uint16_t> barrier_id;
+    uint32_t max_phis = 0;
+    uint32_t rel = 0;
+    for (const BasicBlock& blk : k.blocks) {
+        gevo_block gb{};
+        gb.start = rel;
+        if (blk.instructions.size() > 65535)
+            throw std::invalid_argument("block too long");
+        gb.len = static_cast<uint16_t>(blk.instructions.size());
+        uint16_t nphi = 0;
+        while (nphi < gb.len && blk.instructions[nphi].is_phi())
+            ++nphi;
+        gb.nphi = nphi;
+        max_phis = std::max<uint32_t>(max_phis, nphi);
+        blocks_.push_back(gb);
+        rel += gb.len;
+    }
+    for (const BasicBlock& blk : k.blocks) {
+        for (const Instruction& in : blk.instructions) {
+            gevo_inst g{};
+            g.op = static_cast<uint8_t>(in.op);
+            g.cls = cost_class(k, in);
+            g.res = (in.result && *in.result >= 0) ? static_cast<uint16_t>(slot_of.at(*in.result))
+                                                   : static_cast<uint16_t>(GEVO_NO_RESULT);
+            g.t0 = g.t1 = -1;
+            switch (in.op) {
+            case Opcode::ICmp: case Opcode::FCmp:
+                g.want = static_cast<uint8_t>(in.pred);
+                g.a = ref(in, 0);
+                g.b = ref(in, 1);
+                break;
+            case Opcode::Select:
+                g.want = scalar_tag(in.type.kind);
+                g.a = ref(in, 0);
+                g.b = ref(in, 1);
+                g.c = ref(in, 2);
+                break;
+            case Opcode::Load:
+                g.want = scalar_tag(in.type.kind);
+                g.a = ref(in, 0);
+                g.b = ref(in, 1);
+                break;
+            case Opcode::Store:
+                g.a = ref(in, 0);
+                g.b = ref(in, 1);
+                g.c = ref(in, 2);
+                break;
+            case Opcode::GetIndex:
+                g.want = (in.type.kind == TypeKind::Ptr && in.type.space == MemSpace::Shared) ? 1 : 0;
+                g.a = ref(in, 0);
+                g.b = ref(in, 1);
+                break;
+            case Opcode::Phi: {
+                g.a = static_cast<uint16_t>(arms_.size() - var.arm_base);
+                const size_t n = std::min(in.operands.size(), in.labels.size());
+                // Arms beyond the label list can never match a predecessor.
+                g.b = static_cast<uint16_t>(n);
+                for (size_t a = 0; a < n; ++a)
+                    arms_.push_back(gevo_arm{static_cast<int16_t>(k.block_index(in.labels[a])),
+                                             ref(in, a)});
+                break;
+            }
+            case Opcode::Br:
+                g.want = in.labels.size() == 2 ? 2 : 1;
+                if (!in.labels.empty())
+                    g.t0 = static_cast<int16_t>(k.block_index(in.labels[0]));
+                if (in.labels.size() == 2) {
+                    g.t1 = static_cast<int16_t>(k.block_index(in.labels[1]));
+                    g.a = ref(in, 0);
+                }
+                break;
+            case Opcode::Sync: {
+                const auto it = barrier_id.emplace(in.uid, static_cast<uint16_t>(barrier_id.size()));
+                g.b = it.first->second;
+                var.flags |= GEVO_VAR_HAS_SYNC;
+                break;
+            }
+            case Opcode::Const:
+                g.a = literal(in.const_value);
+                break;
+            case Opcode::Ret: case Opcode::Tid: case Opcode::NThreads:
+                break;
+            default: // two-operand arithmetic
+                g.a = ref(in, 0);
+                g.b = ref(in, 1);
+                break;
+            }
+            insts_.push_back(g);
+        }
+    }
+    var.n_lits = static_cast<uint16_t>(n_lits);
+    var.max_phis = static_cast<uint16_t>(max_phis);
+    var.n_slots = V + P + 2 + n_lits + max_phis;
+    if (var.n_slots > GEVO_MAX_SLOTS)
+        throw std::invalid_argument("variant needs more than GEVO_MAX_SLOTS value slots");
+    for (uint32_t s = V; s < V + P + 2 + n_lits; ++s)
+        slot_ids.push_back(INT32_MIN); // not value ids
+    variants_.push_back(var);
+    slot_value_.push_back(std::move(slot_ids));
+    max_slots_ = std::max(max_slots_, var.n_slots);
+    max_values_ = std::max<uint32_t>(max_values_, V);
+    any_sync_ = any_sync_ || (var.flags & GEVO_VAR_HAS_SYNC);
+    dirty_ = true;
+}
+
+const gevo_batch_header& BatchImage::header() {
+    blob();
+    return hdr_;
+}
+
+const std::vector<uint8_t>& BatchImage::blob() {
+    if (!dirty_)
+        return blob_;
+    auto align = [](uint64_t x) { return (x + 15) & ~uint64_t(15); };
+    gevo_batch_header h{};
+    h.magic = GEVO_MAGIC;
+    h.version = GEVO_VERSION;
+    h.n_variants = static_cast<uint32_t>(variants_.size());
+    h.n_params = static_cast<uint32_t>(suite_.n_params);
+    h.n_insts = static_cast<uint32_t>(insts_.size());
+    h.n_blocks = static_cast<uint32_t>(blocks_.size());
+    h.n_arms = static_cast<uint32_t>(arms_.size());
+    h.n_lits = static_cast<uint32_t>(lit_payload_.size());
+    h.max_slots = max_slots_;
+    h.max_values = max_values_;
+    h.any_sync = any_sync_ ? 1 : 0;
+    uint64_t off = align(sizeof(gevo_batch_header));
+    h.off_variants = off;
+    off = align(off + variants_.size() * sizeof(gevo_variant));
+    h.off_blocks = off;
+    off = align(off + blocks_.size() * sizeof(gevo_block));
+    h.off_insts = off;
+    off = align(off + insts_.size() * sizeof(gevo_inst));
+    h.off_arms = off;
+    off = align(off + arms_.size() * sizeof(gevo_arm));
+    h.off_lit_payload = off;
+    off = align(off + lit_payload_.size() * 4);
+    h.off_lit_tag = off;
+    off = align(off + lit_tag_.size());
+    h.total_bytes = off;
+    blob_.assign(off, 0);
+    std::memcpy(blob_.data(), &h, sizeof h);
+    auto put = [&](uint64_t at, const void* src, size_t n) {
+        if (n)
+            std::memcpy(blob_.data() + at, src, n);
+    };
+    put(h.off_variants, variants_.data(), variants_.size() * sizeof(gevo_variant));
+    put(h.off_blocks, blocks_.data(), blocks_.size() * sizeof(gevo_block));
+    put(h.off_insts, insts_.data(), insts_.size() * sizeof(gevo_inst));
+    put(h.off_arms, arms_.data(), arms_.size() * sizeof(gevo_arm));
+    put(h.off_lit_payload, lit_payload_.data(), lit_payload_.size() * 4);
+    put(h.off_lit_tag, lit_tag_.data(), lit_tag_.size());
+    hdr_ = h;
+    dirty_ = false;
+    return blob_;
+}
+
+std::string reason_text(uint8_t code, const std::string& param_name, int32_t value_id) {
+    switch (code) {
+    case GEVO_TRAP_MISSING_BUFFER: return "missing buffer for param '" + param_name + "'";
+    case GEVO_TRAP_BUFFER_TYPE: return "buffer type mismatch for param '" + param_name + "'";
+    case GEVO_TRAP_MISSING_SCALAR: return "missing scalar for param '" + param_name + "'";
+    case GEVO_TRAP_SCALAR_TYPE: return "scalar type mismatch for param '" + param_name + "'";
+    case GEVO_TRAP_DIVERGENCE: return "barrier divergence";
+    case GEVO_TRAP_BAD_PARAM: return "bad param reference";
+    case GEVO_TRAP_UNDEF_VALUE: return "read of undefined value %" + std::to_string(value_id);
+    case GEVO_TRAP_BAD_OPERAND: return "bad operand";
+    case GEVO_TRAP_OPERAND_TYPE: return "operand type mismatch";
+    case GEVO_TRAP_NOT_POINTER: return "operand is not a pointer";
+    case GEVO_TRAP_SHARED_OOB: return "shared access out of bounds";
+    case GEVO_TRAP_SHARED_UNINIT: return "read of uninitialized shared memory";
+    case GEVO_TRAP_SHARED_TYPE: return "shared load type mismatch";
+    case GEVO_TRAP_GLOBAL_OOB: return "global access out of bounds";
+    case GEVO_TRAP_GLOBAL_LOAD_TYPE: return "global load type mismatch";
+    case GEVO_TRAP_STORE_BOOL: return "store of bool";
+    case GEVO_TRAP_GLOBAL_STORE_TYPE: return "global store type mismatch";
+    case GEVO_TRAP_DEF_NO_ID: return "definition without value id";
+    case GEVO_TRAP_PHI_NO_INCOMING: return "phi has no incoming value for predecessor";
+    case GEVO_TRAP_FELL_OFF: return "fell off the end of a block";
+    case GEVO_TRAP_UNKNOWN_BLOCK: return "branch to unknown block";
+    case GEVO_TRAP_PHI_OUTSIDE: return "phi outside block entry";
+    case GEVO_TRAP_DIV_ZERO: return "integer division by zero";
+    case GEVO_TRAP_DIV_OVERFLOW: return "integer division overflow";
+    case GEVO_TRAP_SELECT_ARM: return "select arm type mismatch";
+    case GEVO_TRAP_STORE_NONSCALAR: return "store of non-scalar";
+    case GEVO_TRAP_GETINDEX_SPACE: return "getindex address space mismatch";
+    case GEVO_TRAP_UNEXPECTED_OP: return "unexpected opcode in straight-line step";
+    case GEVO_BUDGET_EXCEEDED: return "instruction budget exceeded";
+    case GEVO_TRAP_INTERNAL: return "internal interpreter error";
+    default: return "unknown trap " + std::to_string(code);
+    }
+}
+
+std::string BatchImage::reason(size_t v, uint8_t code, int32_t aux) const {
+    std::string pname;
+    int32_t vid = 0;
+    if (code >= GEVO_TRAP_MISSING_BUFFER && code <= GEVO_TRAP_SCALAR_TYPE && aux >= 0 &&
+        aux < suite_.n_params)
+        pname = suite_.param_names[static_cast<size_t>(aux)];
+    if (code == GEVO_TRAP_UNDEF_VALUE && aux >= 0 &&
+        static_cast<size_t>(aux) < slot_value_[v].size())
+        vid = slot_value_[v][static_cast<size_t>(aux)];
+    return reason_text(code, pname, vid);
+}
+
+} // namespace evoir::b200

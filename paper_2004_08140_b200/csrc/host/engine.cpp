@@ -1,0 +1,681 @@
+// Speculative, batched GEVO search engine.
+//
+// Observable behaviour (population, archive, log rows, operator statistics,
+// RNG stream usage) is that of src/engine.cpp of arxiv/paper_2004_08140:
+// stream purposes (19-26), baseline (66-89), sanity_check (91-95), retry loops
+// (97-151), initialisation (153-193), generation step (195-273), archive
+// (275-292), logging (306-332), run + held-out pass + best pick (334-389).
+//
+// What changes is the schedule. A retry loop's k-th attempt draws from the
+// stream left by attempt k-1 and from the (fixed) parent only, so the host
+// draws a wave of attempts per slot ahead of time, recording the stream state
+// after each; all candidates of all slots go to the device as one batch; the
+// first accepted attempt wins and the slot's stream is rewound to the state
+// recorded after it. Statistics count only the attempts the sequential loop
+// would have made.
+#include "evoir/engine.hpp"
+
+#include "runtime.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <exception>
+#include <functional>
+#include <limits>
+#include <mutex>
+#include <thread>
+
+namespace evoir {
+
+namespace {
+
+enum StreamPurpose : uint64_t {
+    kStreamInit = 1,
+    kStreamTournament = 2,
+    kStreamGateCross = 3,
+    kStreamGateMutate = 4,
+    kStreamCross = 5,
+    kStreamMutate = 6,
+};
+
+// Work-sharing loop over [0, n) on up to `jobs` host threads; the first
+// exception is rethrown after all workers stop.
+void host_parallel(size_t n, int jobs, const std::function<void(size_t)>& fn) {
+    if (jobs <= 1 || n <= 1) {
+        for (size_t i = 0; i < n; ++i)
+            fn(i);
+        return;
+    }
+    std::atomic<size_t> next{0};
+    std::atomic<bool> stop{false};
+    std::exception_ptr err;
+    std::mutex mu;
+    std::vector<std::thread> ws;
+    const size_t nw = std::min<size_t>(static_cast<size_t>(jobs), n);
+    for (size_t w = 0; w < nw; ++w)
+        ws.emplace_back([&] {
+            for (;;) {
+                const size_t i = next.fetch_add(1);
+                if (i >= n || stop.load())
+                    return;
+                try {
+                    fn(i);
+                } catch (...) {
+                    std::lock_guard<std::mutex> g(mu);
+                    if (!err)
+                        err = std::current_exception();
+                    stop.store(true);
+                    return;
+                }
+            }
+        });
+    for (auto& t : ws)
+        t.join();
+    if (err)
+        std::rethrow_exception(err);
+}
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// Wave schedule: attempts drawn per slot per round before the next device batch.
+int wave_size(int used, int retries) {
+    const int want = used == 0 ? 6 : (used < 16 ? 12 : 24);
+    return std::max(0, std::min(want, retries - used));
+}
+
+// Device verdicts for a list of kernels (no validation; evaluate_fitness).
+std::vector<EvalOutcome> device_verdicts(b200::DeviceSuite& suite, const b200::ExecImage& ex,
+                                         const std::vector<const Kernel*>& ks, double tol,
+                                         bool with_reasons, EngineCounters& ctr) {
+    std::vector<EvalOutcome> out(ks.size());
+    if (ks.empty())
+        return out;
+    if (suite.image().n_tests == 0) {
+        for (auto& o : out)
+            o = EvalOutcome::rejected(-1, "no test cases");
+        return out;
+    }
+    b200::BatchImage batch(suite.image());
+    for (const Kernel* k : ks)
+        batch.add(*k);
+    b200::EvalOptions opt;
+    opt.tolerance = tol;
+    opt.early_exit = true;
+    const b200::EvalResult r = b200::evaluate(suite, batch, ex, opt);
+    ctr.candidates += static_cast<int64_t>(ks.size());
+    ctr.launches += r.launches;
+    ctr.batches += 1;
+    ctr.device_ms += r.kernel_ms;
+    for (size_t v = 0; v < ks.size(); ++v) {
+        const gevo_variant_record& x = r.variants[v];
+        ctr.executions += x.execs_ref;
+        ctr.dynamic_ir += x.ir_ref;
+        if (x.accepted) {
+            out[v] = EvalOutcome::ok(FitnessVector{x.cost_mean, x.error_max});
+        } else if (!with_reasons) {
+            out[v] = EvalOutcome::rejected(x.failing_test, std::string());
+        } else if (x.code == GEVO_FAIL_TOLERANCE) {
+            out[v] = EvalOutcome::rejected(x.failing_test, "error " + std::to_string(x.fail_error) +
+                                                               " exceeds tolerance");
+        } else {
+            out[v] = EvalOutcome::rejected(x.failing_test, batch.reason(v, x.code, x.aux));
+        }
+    }
+    return out;
+}
+
+} // namespace
+
+// ---------------------------------------------------------------------------
+// Speculation state
+// ---------------------------------------------------------------------------
+
+struct Engine::MutJob {
+    const Individual* parent = nullptr;
+    Rng* rng = nullptr;
+    OperatorStats* stats = nullptr;
+    Individual result;
+    bool done = false;
+    int used = 0;
+    std::unique_ptr<DomTree> dom;
+    std::unique_ptr<MutationContext> ctx;
+    struct Attempt {
+        uint64_t rng_after[4];
+        int kind = -1; // -1: NoCandidate
+        Edit edit;
+        Kernel kernel;
+        bool candidate = false; // applied and valid: goes to the device
+        int verdict = -1;       // index into the wave's verdicts
+    };
+    std::vector<Attempt> wave;
+};
+
+struct Engine::CxJob {
+    const Individual* a = nullptr;
+    const Individual* b = nullptr;
+    Rng* rng = nullptr;
+    OperatorStats* stats = nullptr;
+    Individual ra, rb;
+    bool done = false;
+    int used = 0;
+    struct Attempt {
+        uint64_t rng_after[4];
+        PatchResult pa, pb;
+        int va = -1, vb = -1; // verdict indices, -1: failed validation
+    };
+    std::vector<Attempt> wave;
+};
+
+Engine::Engine(Kernel original, SearchConfig cfg, std::vector<TestCase> tests)
+    : original_(std::move(original)), cfg_(std::move(cfg)), tests_(std::move(tests)) {
+    cfg_.check();
+    if (tests_.empty())
+        throw InitFailure("no test cases");
+    if (!is_valid(original_))
+        throw InitFailure("original kernel fails validation");
+    exec_ = ExecConfig::for_kernel(original_);
+    exec_.instruction_budget = cfg_.instruction_budget;
+    exec_.cost_table = cfg_.cost_table;
+    suite_ = std::make_shared<b200::DeviceSuite>(b200::Device::default_device(),
+                                                 b200::build_suite(original_.params, tests_));
+    exec_img_ = std::make_unique<b200::ExecImage>(b200::exec_image(exec_));
+
+    const EvalOutcome base =
+        device_verdicts(*suite_, *exec_img_, {&original_}, 0.0, true, counters_).at(0);
+    if (!base.accepted)
+        throw InitFailure("original kernel fails its own oracle: " + base.reason);
+    baseline_ = base.fitness;
+    Individual origin;
+    origin.kernel = original_;
+    origin.fitness = baseline_;
+    archive_add(origin);
+}
+
+Engine::~Engine() = default;
+
+EvalOutcome Engine::sanity_check(const Kernel& k) const {
+    return sanity_check_batch({&k}, true).at(0);
+}
+
+std::vector<EvalOutcome> Engine::sanity_check_batch(const std::vector<const Kernel*>& ks,
+                                                    bool with_reasons) const {
+    std::vector<EvalOutcome> out(ks.size());
+    std::vector<char> ok(ks.size(), 0);
+    host_parallel(ks.size(), cfg_.jobs, [&](size_t i) { ok[i] = is_valid(*ks[i]) ? 1 : 0; });
+    std::vector<const Kernel*> dev;
+    std::vector<size_t> where;
+    for (size_t i = 0; i < ks.size(); ++i) {
+        if (!ok[i]) {
+            out[i] = EvalOutcome::rejected(-1, "validation failed");
+            continue;
+        }
+        dev.push_back(ks[i]);
+        where.push_back(i);
+    }
+    const auto v = device_verdicts(*suite_, *exec_img_, dev, cfg_.tolerance, with_reasons, counters_);
+    for (size_t j = 0; j < where.size(); ++j)
+        out[where[j]] = v[j];
+    return out;
+}
+
+void Engine::run_mutations(std::vector<MutJob>& jobs) const {
+    const int retries = cfg_.mutation_retries;
+    for (MutJob& j : jobs) {
+        if (retries <= 0) {
+            ++j.stats->mut_exhausted;
+            j.result = *j.parent;
+            j.done = true;
+        }
+    }
+    for (;;) {
+        std::vector<MutJob*> active;
+        for (MutJob& j : jobs)
+            if (!j.done)
+                active.push_back(&j);
+        if (active.empty())
+            return;
+        const auto t0 = std::chrono::steady_clock::now();
+        // 1. draw, apply and validate a wave of attempts per active slot
+        host_parallel(active.size(), cfg_.jobs, [&](size_t i) {
+            MutJob& j = *active[i];
+            if (!j.ctx) {
+                j.dom = std::make_unique<DomTree>(DomTree::build(j.parent->kernel));
+                j.ctx = std::make_unique<MutationContext>(j.parent->kernel, *j.dom, *j.rng);
+            }
+            j.wave.clear();
+            const int k = wave_size(j.used, retries);
+            j.wave.resize(static_cast<size_t>(k));
+            for (int a = 0; a < k; ++a) {
+                MutJob::Attempt& at = j.wave[static_cast<size_t>(a)];
+                MutationResult m = random_mutation(*j.ctx);
+                j.rng->get_state(at.rng_after);
+                if (!m)
+                    continue;
+                at.kind = static_cast<int>(operator_kind(*m));
+                at.edit = std::move(*m);
+                ApplyResult ap = apply_edit(j.parent->kernel, at.edit);
+                if (!ap.applied)
+                    continue;
+                at.kernel = std::move(ap.kernel);
+                at.candidate = is_valid(at.kernel);
+            }
+        });
+        // 2. one device batch for every candidate of every slot
+        std::vector<const Kernel*> ks;
+        for (MutJob* j : active)
+            for (auto& at : j->wave)
+                if (at.candidate) {
+                    at.verdict = static_cast<int>(ks.size());
+                    ks.push_back(&at.kernel);
+                }
+        counters_.host_gen_ms += ms_since(t0);
+        const auto verdicts =
+            device_verdicts(*suite_, *exec_img_, ks, cfg_.tolerance, false, counters_);
+        // 3. resolve each slot in attempt order
+        for (MutJob* j : active) {
+            for (auto& at : j->wave) {
+                ++j->used;
+                if (at.kind < 0)
+                    continue;
+                ++j->stats->attempts[at.kind];
+                if (!at.candidate || !verdicts[static_cast<size_t>(at.verdict)].accepted)
+                    continue;
+                ++j->stats->accepts[at.kind];
+                Individual next;
+                next.kernel = std::move(at.kernel);
+                next.patch = j->parent->patch;
+                next.patch.push_back(at.edit);
+                next.fitness = verdicts[static_cast<size_t>(at.verdict)].fitness;
+                j->result = std::move(next);
+                j->rng->set_state(at.rng_after);
+                j->done = true;
+                break;
+            }
+            if (!j->done && j->used >= retries) {
+                ++j->stats->mut_exhausted;
+                j->result = *j->parent;
+                j->done = true;
+            }
+            j->wave.clear();
+        }
+    }
+}
+
+void Engine::run_crossovers(std::vector<CxJob>& jobs) const {
+    const int retries = cfg_.crossover_retries;
+    for (CxJob& j : jobs) {
+        if (retries <= 0) {
+            ++j.stats->cx_exhausted;
+            j.ra = *j.a;
+            j.rb = *j.b;
+            j.done = true;
+        }
+    }
+    for (;;) {
+        std::vector<CxJob*> active;
+        for (CxJob& j : jobs)
+            if (!j.done)
+                active.push_back(&j);
+        if (active.empty())
+            return;
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::vector<char>> valid(active.size());
+        host_parallel(active.size(), cfg_.jobs, [&](size_t i) {
+            CxJob& j = *active[i];
+            j.wave.clear();
+            const int k = std::min(j.used == 0 ? 4 : 8, retries - j.used);
+            j.wave.resize(static_cast<size_t>(k));
+            valid[i].assign(2 * static_cast<size_t>(k), 0);
+            for (int a = 0; a < k; ++a) {
+                CxJob::Attempt& at = j.wave[static_cast<size_t>(a)];
+                auto [pa, pb] = crossover_messy(j.a->patch, j.b->patch, *j.rng);
+                j.rng->get_state(at.rng_after);
+                at.pa = apply_patch(original_, pa);
+                at.pb = apply_patch(original_, pb);
+                valid[i][2 * a] = is_valid(at.pa.kernel) ? 1 : 0;
+                valid[i][2 * a + 1] = is_valid(at.pb.kernel) ? 1 : 0;
+            }
+        });
+        std::vector<const Kernel*> ks;
+        for (size_t i = 0; i < active.size(); ++i)
+            for (size_t a = 0; a < active[i]->wave.size(); ++a) {
+                auto& at = active[i]->wave[a];
+                if (valid[i][2 * a]) {
+                    at.va = static_cast<int>(ks.size());
+                    ks.push_back(&at.pa.kernel);
+                }
+                if (valid[i][2 * a + 1]) {
+                    at.vb = static_cast<int>(ks.size());
+                    ks.push_back(&at.pb.kernel);
+                }
+            }
+        counters_.host_gen_ms += ms_since(t0);
+        const auto verdicts =
+            device_verdicts(*suite_, *exec_img_, ks, cfg_.tolerance, false, counters_);
+        for (CxJob* j : active) {
+            for (auto& at : j->wave) {
+                ++j->used;
+                ++j->stats->cx_attempts;
+                if (at.va < 0 || !verdicts[static_cast<size_t>(at.va)].accepted)
+                    continue;
+                if (at.vb < 0 || !verdicts[static_cast<size_t>(at.vb)].accepted)
+                    continue;
+                ++j->stats->cx_accepts;
+                j->ra.kernel = std::move(at.pa.kernel);
+                j->ra.patch = std::move(at.pa.applied);
+                j->ra.fitness = verdicts[static_cast<size_t>(at.va)].fitness;
+                j->rb.kernel = std::move(at.pb.kernel);
+                j->rb.patch = std::move(at.pb.applied);
+                j->rb.fitness = verdicts[static_cast<size_t>(at.vb)].fitness;
+                j->rng->set_state(at.rng_after);
+                j->done = true;
+                break;
+            }
+            if (!j->done && j->used >= retries) {
+                ++j->stats->cx_exhausted;
+                j->ra = *j->a;
+                j->rb = *j->b;
+                j->done = true;
+            }
+            j->wave.clear();
+        }
+    }
+}
+
+Individual Engine::mutate_until_valid(const Individual& ind, Rng& rng, OperatorStats& stats) const {
+    std::vector<MutJob> jobs(1);
+    jobs[0].parent = &ind;
+    jobs[0].rng = &rng;
+    jobs[0].stats = &stats;
+    run_mutations(jobs);
+    return std::move(jobs[0].result);
+}
+
+std::pair<Individual, Individual> Engine::crossover_until_valid(const Individual& a,
+                                                                const Individual& b, Rng& rng,
+                                                                OperatorStats& stats) const {
+    std::vector<CxJob> jobs(1);
+    jobs[0].a = &a;
+    jobs[0].b = &b;
+    jobs[0].rng = &rng;
+    jobs[0].stats = &stats;
+    run_crossovers(jobs);
+    return {std::move(jobs[0].ra), std::move(jobs[0].rb)};
+}
+
+void Engine::initialize_population() {
+    const size_t pop = static_cast<size_t>(cfg_.pop_size);
+    std::vector<Individual> cur(pop);
+    std::vector<Rng> rngs;
+    rngs.reserve(pop);
+    for (size_t s = 0; s < pop; ++s) {
+        cur[s].kernel = original_;
+        cur[s].fitness = baseline_;
+        rngs.push_back(Rng::stream(cfg_.master_seed, 0, s, kStreamInit));
+    }
+    std::vector<OperatorStats> slot_stats(pop);
+    std::vector<std::string> failures(pop);
+    std::vector<char> alive(pop, 1);
+    for (int m = 0; m < cfg_.init_dist; ++m) {
+        std::vector<MutJob> jobs;
+        std::vector<size_t> slots;
+        for (size_t s = 0; s < pop; ++s)
+            if (alive[s]) {
+                jobs.emplace_back();
+                jobs.back().parent = &cur[s];
+                jobs.back().rng = &rngs[s];
+                jobs.back().stats = &slot_stats[s];
+                slots.push_back(s);
+            }
+        if (jobs.empty())
+            break;
+        run_mutations(jobs);
+        for (size_t i = 0; i < jobs.size(); ++i) {
+            const size_t s = slots[i];
+            if (jobs[i].result.patch.size() == cur[s].patch.size()) {
+                failures[s] = "initialization slot " + std::to_string(s) +
+                              " exhausted mutation retries at distance " + std::to_string(m);
+                alive[s] = 0;
+                continue;
+            }
+            cur[s] = std::move(jobs[i].result);
+        }
+    }
+    population_.assign(pop, Individual{});
+    for (size_t s = 0; s < pop; ++s)
+        if (alive[s])
+            population_[s] = std::move(cur[s]);
+
+    OperatorStats init_stats;
+    for (const auto& st : slot_stats)
+        init_stats.merge(st);
+    stats_.merge(init_stats);
+    for (const auto& f : failures)
+        if (!f.empty()) {
+            std::string detail = f + " (attempts:";
+            for (int i = 0; i < kOperatorCount; ++i)
+                detail += " " + std::string(operator_kind_name(static_cast<OperatorKind>(i))) + "=" +
+                          std::to_string(init_stats.attempts[i]);
+            throw InitFailure(detail + ")");
+        }
+    for (const auto& ind : population_)
+        archive_add(ind);
+    rank_current();
+    generation_ = 0;
+    log_generation(init_stats);
+}
+
+void Engine::step_generation() {
+    const size_t pop = static_cast<size_t>(cfg_.pop_size);
+    const uint64_t gen = static_cast<uint64_t>(generation_) + 1;
+
+    Rng trng = Rng::stream(cfg_.master_seed, gen, 0, kStreamTournament);
+    const std::vector<int> off_idx = tournament_select(rank_, population_.size(), pop, trng);
+    const std::vector<int> elite_idx = select_best(rank_, pop / 4);
+    std::vector<Individual> offspring;
+    offspring.reserve(pop);
+    for (int i : off_idx)
+        offspring.push_back(population_[static_cast<size_t>(i)]);
+    std::vector<Individual> elites;
+    elites.reserve(elite_idx.size());
+    for (int i : elite_idx)
+        elites.push_back(population_[static_cast<size_t>(i)]);
+
+    Rng gx = Rng::stream(cfg_.master_seed, gen, 0, kStreamGateCross);
+    Rng gm = Rng::stream(cfg_.master_seed, gen, 0, kStreamGateMutate);
+    std::vector<char> cx_fire(pop / 2), mut_fire(pop);
+    for (auto& f : cx_fire)
+        f = gx.chance(cfg_.cross_rate) ? 1 : 0;
+    for (auto& f : mut_fire)
+        f = gm.chance(cfg_.mutate_rate) ? 1 : 0;
+
+    // Crossover: every firing pair is one speculative job.
+    std::vector<OperatorStats> pair_stats(pop / 2);
+    {
+        std::vector<Rng> rngs;
+        std::vector<CxJob> jobs;
+        std::vector<size_t> pairs;
+        for (size_t p = 0; p < pop / 2; ++p)
+            if (cx_fire[p]) {
+                pairs.push_back(p);
+                rngs.push_back(Rng::stream(cfg_.master_seed, gen, p, kStreamCross));
+            }
+        jobs.resize(pairs.size());
+        for (size_t i = 0; i < pairs.size(); ++i) {
+            jobs[i].a = &offspring[2 * pairs[i]];
+            jobs[i].b = &offspring[2 * pairs[i] + 1];
+            jobs[i].rng = &rngs[i];
+            jobs[i].stats = &pair_stats[pairs[i]];
+        }
+        run_crossovers(jobs);
+        for (size_t i = 0; i < pairs.size(); ++i) {
+            offspring[2 * pairs[i]] = std::move(jobs[i].ra);
+            offspring[2 * pairs[i] + 1] = std::move(jobs[i].rb);
+        }
+    }
+    // Mutation: every firing slot is one speculative job.
+    std::vector<OperatorStats> mut_stats(pop);
+    {
+        std::vector<Rng> rngs;
+        std::vector<MutJob> jobs;
+        std::vector<size_t> slots;
+        for (size_t i = 0; i < pop; ++i)
+            if (mut_fire[i]) {
+                slots.push_back(i);
+                rngs.push_back(Rng::stream(cfg_.master_seed, gen, i, kStreamMutate));
+            }
+        jobs.resize(slots.size());
+        std::vector<Individual> parents(slots.size());
+        for (size_t i = 0; i < slots.size(); ++i)
+            parents[i] = offspring[slots[i]];
+        for (size_t i = 0; i < slots.size(); ++i) {
+            jobs[i].parent = &parents[i];
+            jobs[i].rng = &rngs[i];
+            jobs[i].stats = &mut_stats[slots[i]];
+        }
+        run_mutations(jobs);
+        for (size_t i = 0; i < slots.size(); ++i)
+            offspring[slots[i]] = std::move(jobs[i].result);
+    }
+
+    OperatorStats gen_stats;
+    for (const auto& s : pair_stats)
+        gen_stats.merge(s);
+    for (const auto& s : mut_stats)
+        gen_stats.merge(s);
+    stats_.merge(gen_stats);
+
+    std::vector<Individual> pool = std::move(elites);
+    for (auto& ind : offspring)
+        pool.push_back(std::move(ind));
+    std::vector<FitnessVector> fits;
+    fits.reserve(pool.size());
+    for (const auto& ind : pool)
+        fits.push_back(*ind.fitness);
+    const ParetoRank pool_rank = rank_population(fits);
+    const std::vector<int> keep = select_best(pool_rank, pop);
+    std::vector<Individual> next;
+    next.reserve(pop);
+    for (int i : keep)
+        next.push_back(std::move(pool[static_cast<size_t>(i)]));
+    population_ = std::move(next);
+    for (const auto& ind : population_)
+        archive_add(ind);
+    rank_current();
+    ++generation_;
+    log_generation(gen_stats);
+}
+
+void Engine::archive_add(const Individual& ind) {
+    if (!ind.fitness)
+        return;
+    const FitnessVector f = *ind.fitness;
+    for (const auto& e : archive_) {
+        const FitnessVector& g = *e.ind.fitness;
+        if (g == f || dominates(g, f))
+            return;
+    }
+    archive_.erase(std::remove_if(archive_.begin(), archive_.end(),
+                                  [&](const ArchiveEntry& e) { return dominates(f, *e.ind.fitness); }),
+                   archive_.end());
+    ArchiveEntry e;
+    e.ind = ind;
+    archive_.push_back(std::move(e));
+}
+
+void Engine::rank_current() { rank_ = rank_population(population_fitness()); }
+
+std::vector<FitnessVector> Engine::population_fitness() const {
+    std::vector<FitnessVector> fits;
+    fits.reserve(population_.size());
+    for (const auto& ind : population_)
+        fits.push_back(*ind.fitness);
+    return fits;
+}
+
+void Engine::log_generation(const OperatorStats& gs) {
+    GenerationLog row;
+    row.gen = generation_;
+    const double inf = std::numeric_limits<double>::infinity();
+    double b0 = inf, bt = inf, me = inf;
+    auto see = [&](const FitnessVector& f) {
+        if (f.error == 0.0)
+            b0 = std::min(b0, f.cost);
+        bt = std::min(bt, f.cost);
+        me = std::min(me, f.error);
+    };
+    for (const auto& ind : population_)
+        see(*ind.fitness);
+    for (const auto& e : archive_)
+        see(*e.ind.fitness);
+    row.best_cost_err0 = b0;
+    row.best_cost_tol = bt;
+    row.min_error = me;
+    row.front0_size = rank_.fronts.empty() ? 0 : static_cast<int>(rank_.fronts[0].size());
+    row.mut_attempts = gs.total_attempts();
+    row.mut_accepts = gs.total_accepts();
+    row.cx_attempts = gs.cx_attempts;
+    row.cx_accepts = gs.cx_accepts;
+    log_.push_back(row);
+}
+
+SearchResult Engine::run(const std::vector<TestCase>& heldout) {
+    initialize_population();
+    if (cfg_.budget.kind == Budget::Kind::Generations) {
+        for (int g = 0; g < cfg_.budget.generations; ++g)
+            step_generation();
+    } else {
+        const auto start = std::chrono::steady_clock::now();
+        while (ms_since(start) / 1000.0 < cfg_.budget.seconds)
+            step_generation();
+    }
+    if (!heldout.empty()) {
+        b200::DeviceSuite hs(b200::Device::default_device(),
+                             b200::build_suite(original_.params, heldout));
+        std::vector<const Kernel*> ks;
+        for (const auto& e : archive_)
+            ks.push_back(&e.ind.kernel);
+        const auto v = device_verdicts(hs, *exec_img_, ks, cfg_.tolerance, false, counters_);
+        for (size_t i = 0; i < archive_.size(); ++i) {
+            if (v[i].accepted) {
+                archive_[i].heldout_error = v[i].fitness.error;
+                archive_[i].overfit = false;
+            } else {
+                archive_[i].heldout_error = 1.0;
+                archive_[i].overfit = true;
+            }
+        }
+    }
+    SearchResult r;
+    r.population = population_;
+    r.archive = archive_;
+    r.log = log_;
+    r.stats = stats_;
+    r.baseline = baseline_;
+    r.generations_run = generation_;
+    for (size_t i = 0; i < r.archive.size(); ++i) {
+        const ArchiveEntry& e = r.archive[i];
+        if (e.overfit)
+            continue;
+        if (r.best_index < 0) {
+            r.best_index = static_cast<int>(i);
+            continue;
+        }
+        const FitnessVector& best = *r.archive[static_cast<size_t>(r.best_index)].ind.fitness;
+        const FitnessVector& c = *e.ind.fitness;
+        if (c.cost < best.cost || (c.cost == best.cost && c.error < best.error))
+            r.best_index = static_cast<int>(i);
+    }
+    return r;
+}
+
+SearchResult run_search(const Kernel& original, const SearchConfig& cfg,
+                        const std::vector<TestCase>& tests, const std::vector<TestCase>& heldout) {
+    Engine engine(original, cfg, tests);
+    return engine.run(heldout);
+}
+
+} // namespace evoir

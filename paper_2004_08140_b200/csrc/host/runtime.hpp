@@ -1,0 +1,90 @@
+// Device runtime: context (device + stream + reusable buffers), test suites
+// resident in HBM, batch evaluation and GPU ranking. Host code only sees
+// plain records; CUDA types stay behind this header.
+#pragma once
+
+#include "encode.hpp"
+#include "evoir/nsga.hpp"
+
+#include <memory>
+#include <mutex>
+#include <vector>
+
+namespace evoir::b200 {
+
+struct DeviceImpl;
+struct SuiteImpl;
+
+class Device {
+public:
+    // Throws DeviceUnavailable when CUDA has no device.
+    explicit Device(int ordinal = -1);
+    ~Device();
+    Device(const Device&) = delete;
+    Device& operator=(const Device&) = delete;
+
+    int ordinal() const;
+    DeviceImpl& impl() { return *impl_; }
+    std::mutex& lock() { return mu_; }
+
+    // Process-wide default device (GEVO_DEVICE env or the current CUDA device).
+    static Device& default_device();
+
+private:
+    std::unique_ptr<DeviceImpl> impl_;
+    std::mutex mu_;
+};
+
+// A test suite uploaded to one device (inputs, oracles, binding tables).
+class DeviceSuite {
+public:
+    DeviceSuite(Device& dev, SuiteImage image);
+    ~DeviceSuite();
+    const SuiteImage& image() const { return image_; }
+    SuiteImpl& impl() { return *impl_; }
+    Device& device() { return dev_; }
+
+private:
+    Device& dev_;
+    SuiteImage image_;
+    std::unique_ptr<SuiteImpl> impl_;
+};
+
+struct EvalOptions {
+    double tolerance = 0.0;
+    bool early_exit = false;      // skip tests after a variant's first failure
+    bool want_tests = false;      // copy per-test records back
+    bool want_outputs = false;    // copy final global buffers back (small batches)
+};
+
+struct EvalResult {
+    std::vector<gevo_variant_record> variants;
+    std::vector<gevo_test_record> tests;          // [variant * n_tests + test] when requested
+    std::vector<std::vector<BufferMap>> outputs;  // [variant][test] when requested
+    float kernel_ms = 0.0f;                       // interpreter + reduction, CUDA events
+    uint64_t h2d_bytes = 0;
+    uint64_t d2h_bytes = 0;
+    int launches = 0;
+};
+
+// Evaluates every variant of `batch` on every test of `suite`.
+EvalResult evaluate(DeviceSuite& suite, BatchImage& batch, const ExecImage& exec,
+                    const EvalOptions& opt);
+
+// Device-resident variant for benchmarks: the blob is uploaded once and
+// re-evaluated without host transfers of programs.
+struct ResidentBatch;
+std::shared_ptr<ResidentBatch> make_resident(DeviceSuite& suite, BatchImage& batch);
+// Runs the interpreter + reduction on a resident batch; returns kernel ms
+// (CUDA events on the launch stream) and fills `interp_ms` with the share of
+// the interpreter kernel alone.
+float evaluate_resident(ResidentBatch& rb, const ExecImage& exec, const EvalOptions& opt,
+                        float* interp_ms, std::vector<gevo_variant_record>* out);
+
+// GPU NSGA ranking (front + crowding + fronts in reference order).
+ParetoRank rank_on_device(Device& dev, const std::vector<FitnessVector>& fits, bool single_group);
+
+// compute_error of two host buffer maps, evaluated by the device metric.
+double error_on_device(Device& dev, const BufferMap& candidate, const BufferMap& oracle);
+
+} // namespace evoir::b200
