@@ -306,12 +306,15 @@ static void parse_inst(Cur* c, const eo_kernel* k, Inst* in) {
         break;
     case OP_BR: {
         ws(c);
-        size_t save = c->p;
-        char* id = ident(c);
-        ws(c);
-        int cond = c->s[c->p] == ',';
-        c->p = save;
-        free(id);
+        int cond = c->s[c->p] == '%' || isdigit((unsigned char)c->s[c->p]);
+        if (!cond) {
+            size_t save = c->p;
+            char* id = ident(c);
+            ws(c);
+            cond = c->s[c->p] == ',';
+            c->p = save;
+            free(id);
+        }
         if (cond) {
             push_op(in, operand(c, k));
             need(c, ',');
