@@ -59,6 +59,10 @@ typedef struct gevo_batch gevo_batch;
 int gevo_abi_version(void);
 int gevo_device_count(void);
 const char* gevo_last_error(void);
+/* Launch all work of the default device on a caller-owned cudaStream_t
+ * (passed as void*; NULL restores the library's own stream), so a caller's
+ * CUDA events bracket the library's launches. No reference counterpart. */
+int gevo_set_stream(void* stream);
 void gevo_free(void* p);
 
 /* ---- test suites (uploaded once, resident in HBM) ------------------------
@@ -153,6 +157,13 @@ int gevo_random_mutation(const char* kernel_ir, uint64_t master, uint64_t a, uin
 int gevo_benchmark_inputs(const char* bench, int count, uint64_t seed, char** tests_json);
 int gevo_benchmark_names(char** names_json);
 int gevo_benchmark_ir(const char* bench, char** ir);
+/* Bench/sweep workload: n validated mutants of a registry benchmark, drawn
+ * as seeded random walks of up to max_depth accepted-by-validate edits
+ * (random_mutation + apply_edit + validate, src/operators.cpp:348,
+ * src/genome.cpp:212, src/validate.cpp:324), one compact patch JSON per line.
+ * No evaluation: the mix keeps trapping, spinning and over-tolerance
+ * variants, as the search's candidate stream does. */
+int gevo_sample_candidates(const char* bench, int n, uint64_t seed, int max_depth, char** patches);
 /* Train / held-out suite seeds (src/cli_app.cpp:193-201). */
 uint64_t gevo_train_seed(uint64_t master);
 uint64_t gevo_heldout_seed(uint64_t master);

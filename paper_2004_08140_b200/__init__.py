@@ -93,6 +93,7 @@ _SIGNATURES = [
     ("gevo_abi_version", ctypes.c_int, []),
     ("gevo_device_count", ctypes.c_int, []),
     ("gevo_last_error", ctypes.c_char_p, []),
+    ("gevo_set_stream", ctypes.c_int, [_vp]),
     ("gevo_free", None, [_vp]),
     ("gevo_suite_from_benchmark", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _u64, ctypes.c_int,
                                                  ctypes.POINTER(_vp)]),
@@ -133,6 +134,8 @@ _SIGNATURES = [
     ("gevo_benchmark_inputs", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _u64, _str_out]),
     ("gevo_benchmark_names", ctypes.c_int, [_str_out]),
     ("gevo_benchmark_ir", ctypes.c_int, [ctypes.c_char_p, _str_out]),
+    ("gevo_sample_candidates", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _u64, ctypes.c_int,
+                                              _str_out]),
     ("gevo_train_seed", _u64, [_u64]),
     ("gevo_heldout_seed", _u64, [_u64]),
     ("gevo_run_search", ctypes.c_int, [ctypes.c_char_p, _u64, ctypes.c_int, ctypes.c_int,
@@ -228,6 +231,18 @@ def benchmark_inputs(name: str, count: int, seed: int) -> list:
     out = ctypes.c_void_p()
     _check(lib().gevo_benchmark_inputs(_b(name), count, seed, ctypes.byref(out)))
     return json.loads(_take(out))
+
+
+def sample_candidates(bench: str, n: int, seed: int, max_depth: int = 4) -> list:
+    """n validated (not evaluated) mutants of `bench` as patch JSON strings."""
+    out = ctypes.c_void_p()
+    _check(lib().gevo_sample_candidates(_b(bench), n, seed, max_depth, ctypes.byref(out)))
+    return [line for line in _take(out).split("\n") if line]
+
+
+def set_stream(stream_ptr: int) -> None:
+    """Run the library's launches on a caller's CUDA stream (0 = its own)."""
+    _check(lib().gevo_set_stream(ctypes.c_void_p(stream_ptr or None)))
 
 
 def train_seed(master: int) -> int:

@@ -3,6 +3,7 @@
 
 #include "evoir/cli_app.hpp"
 #include "evoir/corpus.hpp"
+#include "evoir/operators.hpp"
 #include "host/runtime.hpp"
 
 #include <json.hpp>
@@ -133,6 +134,10 @@ int gevo_device_count(void) {
         return 0;
     n = 1;
     return n;
+}
+
+int gevo_set_stream(void* stream) {
+    return guard([&] { b200::Device::default_device().set_stream(stream); });
 }
 
 const char* gevo_last_error(void) { return g_error.c_str(); }
@@ -453,6 +458,45 @@ int gevo_benchmark_names(char** names_json) {
 
 int gevo_benchmark_ir(const char* bench, char** ir) {
     return guard([&] { *ir = dup(print_kernel(load_benchmark(bench).kernel)); });
+}
+
+int gevo_sample_candidates(const char* bench, int n, uint64_t seed, int max_depth,
+                           char** patches) {
+    return guard([&] {
+        if (n < 0 || max_depth < 1)
+            throw std::invalid_argument("gevo_sample_candidates: n >= 0 and max_depth >= 1");
+        const Benchmark b = load_benchmark(bench);
+        struct Parent {
+            Kernel k;
+            Patch p;
+        };
+        std::vector<Parent> parents{{b.kernel, {}}};
+        Rng pick(seed ^ 0xCA7D1DA7E5ULL);
+        std::string out;
+        int made = 0;
+        for (uint64_t i = 0; made < n; ++i) {
+            if (i > static_cast<uint64_t>(n) * 200 + 1000)
+                throw std::invalid_argument("gevo_sample_candidates: kernel yields no valid mutants");
+            const Parent& par = parents[pick.index(parents.size())];
+            Rng rng = Rng::stream(seed, 0xC4, i, 1);
+            const DomTree dom = DomTree::build(par.k);
+            MutationContext ctx(par.k, dom, rng);
+            const MutationResult m = random_mutation(ctx);
+            if (!m)
+                continue;
+            ApplyResult ar = apply_edit(par.k, *m);
+            if (!ar.applied || !is_valid(ar.kernel))
+                continue;
+            Patch p = par.p;
+            p.push_back(*m);
+            out += nlohmann::json::parse(patch_to_json(p)).dump();
+            out += '\n';
+            ++made;
+            if (static_cast<int>(p.size()) < max_depth)
+                parents.push_back({std::move(ar.kernel), std::move(p)});
+        }
+        *patches = dup(out);
+    });
 }
 
 uint64_t gevo_train_seed(uint64_t master) { return cli::train_seed(master); }

@@ -68,6 +68,7 @@ struct PinnedBuf {
 struct DeviceImpl {
     int ordinal = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr; // created here; `stream` may be a caller's
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     DevBuf blob, rec, vrec, first_fail, priv, sh_tag, sh_val;
     DevBuf ts_pos, ts_prev, ts_exec, ts_stop, ts_val, ts_tag;
@@ -96,21 +97,27 @@ Device::Device(int ordinal) : impl_(std::make_unique<DeviceImpl>()) {
     }
     impl_->ordinal = ordinal;
     check(cudaSetDevice(ordinal), "cudaSetDevice");
-    check(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    check(cudaStreamCreateWithFlags(&impl_->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    impl_->stream = impl_->own_stream;
     check(cudaEventCreate(&impl_->ev0), "cudaEventCreate");
     check(cudaEventCreate(&impl_->ev1), "cudaEventCreate");
     check(cudaEventCreate(&impl_->ev2), "cudaEventCreate");
 }
 
 Device::~Device() {
-    if (impl_->stream)
-        cudaStreamDestroy(impl_->stream);
+    if (impl_->own_stream)
+        cudaStreamDestroy(impl_->own_stream);
     cudaEventDestroy(impl_->ev0);
     cudaEventDestroy(impl_->ev1);
     cudaEventDestroy(impl_->ev2);
 }
 
 int Device::ordinal() const { return impl_->ordinal; }
+
+void Device::set_stream(void* stream) {
+    std::lock_guard<std::mutex> g(mu_);
+    impl_->stream = stream ? static_cast<cudaStream_t>(stream) : impl_->own_stream;
+}
 
 Device& Device::default_device() {
     static Device* dev = new Device(-1); // intentionally leaked: outlives static teardown

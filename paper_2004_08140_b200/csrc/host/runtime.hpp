@@ -24,6 +24,8 @@ public:
     Device& operator=(const Device&) = delete;
 
     int ordinal() const;
+    // Launch on a caller-owned stream (nullptr: back to the device's own).
+    void set_stream(void* stream);
     DeviceImpl& impl() { return *impl_; }
     std::mutex& lock() { return mu_; }
 
