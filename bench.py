@@ -228,6 +228,7 @@ def b200_arm(args):
         b.make_resident()
         batches[k] = b
 
+    gevo.spin_counters(reset=True)
     # One untimed pass with per-test records: device-executed IR (speculative
     # work included) for the issue-rate roofline.
     dev_ir = 0
@@ -238,6 +239,7 @@ def b200_arm(args):
         ref_execs_step += int(v["execs_ref"].sum())
         ref_ir_step += int(v["ir_ref"].sum())
 
+    spins = gevo.spin_counters(reset=True)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
     gathered_front = None
@@ -378,6 +380,8 @@ def b200_arm(args):
         "cpu_baseline": cpu,
         "clocks": ck,
         "step_ms": [round(x, 4) for x in step_ms],
+        "spin_accelerator": {"loops_jumped_per_step": spins[0],
+                             "instructions_skipped_per_step": spins[1]},
     }
     print(json.dumps(line))
     if world > 1:

@@ -63,6 +63,10 @@ const char* gevo_last_error(void);
  * (passed as void*; NULL restores the library's own stream), so a caller's
  * CUDA events bracket the library's launches. No reference counterpart. */
 int gevo_set_stream(void* stream);
+/* Diagnostics of the exact spin accelerator on the default device since the
+ * last reset: out2[0] = budget-bound loops jumped, out2[1] = instructions
+ * skipped by those jumps (counted in the records as executed). */
+int gevo_spin_counters(uint64_t* out2, int reset);
 void gevo_free(void* p);
 
 /* ---- test suites (uploaded once, resident in HBM) ------------------------

@@ -94,6 +94,7 @@ _SIGNATURES = [
     ("gevo_device_count", ctypes.c_int, []),
     ("gevo_last_error", ctypes.c_char_p, []),
     ("gevo_set_stream", ctypes.c_int, [_vp]),
+    ("gevo_spin_counters", ctypes.c_int, [_vp, ctypes.c_int]),
     ("gevo_free", None, [_vp]),
     ("gevo_suite_from_benchmark", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _u64, ctypes.c_int,
                                                  ctypes.POINTER(_vp)]),
@@ -243,6 +244,13 @@ def sample_candidates(bench: str, n: int, seed: int, max_depth: int = 4) -> list
 def set_stream(stream_ptr: int) -> None:
     """Run the library's launches on a caller's CUDA stream (0 = its own)."""
     _check(lib().gevo_set_stream(ctypes.c_void_p(stream_ptr or None)))
+
+
+def spin_counters(reset: bool = False) -> tuple:
+    """(loops jumped, instructions skipped) by the spin accelerator."""
+    out = (ctypes.c_uint64 * 2)()
+    _check(lib().gevo_spin_counters(ctypes.cast(out, ctypes.c_void_p), 1 if reset else 0))
+    return out[0], out[1]
 
 
 def train_seed(master: int) -> int:

@@ -140,6 +140,10 @@ int gevo_set_stream(void* stream) {
     return guard([&] { b200::Device::default_device().set_stream(stream); });
 }
 
+int gevo_spin_counters(uint64_t* out2, int reset) {
+    return guard([&] { b200::spin_counters(b200::Device::default_device(), out2, reset != 0); });
+}
+
 const char* gevo_last_error(void) { return g_error.c_str(); }
 
 void gevo_free(void* p) { std::free(p); }
@@ -259,11 +263,13 @@ int gevo_eval_resident(gevo_batch* b, const gevo_exec_config* cfg, double tolera
         opt.early_exit = (flags & GEVO_EVAL_EARLY_EXIT) != 0;
         std::vector<gevo_variant_record> recs;
         float interp = 0.0f;
+        int launches = 0;
         const float ms = b200::evaluate_resident(*b->resident, b200::exec_image(exec_from(cfg)), opt,
-                                                 &interp, out_variants ? &recs : nullptr);
+                                                 &interp, out_variants ? &recs : nullptr, &launches);
         if (out_variants && !recs.empty())
             std::memcpy(out_variants, recs.data(), recs.size() * sizeof(gevo_variant_record));
-        fill_stats(stats, ms, 0, out_variants ? recs.size() * sizeof(gevo_variant_record) : 0, 2);
+        fill_stats(stats, ms, 0, out_variants ? recs.size() * sizeof(gevo_variant_record) : 0,
+                   launches);
     });
 }
 

@@ -112,20 +112,22 @@ enum { GEVO_STATUS_COMPLETED = 0, GEVO_STATUS_TRAP = 1, GEVO_STATUS_BUDGET = 2,
 #define GEVO_MAX_PARAMS 48
 #define GEVO_MAX_SLOTS 1400
 
-/* 16-byte instruction record. */
+/* 16-byte instruction record, laid out for a cheap decode on the device:
+ * word 0 = op | aux << 8 | otag << 16 | cls << 24, word 1 = a | b << 16,
+ * word 2 = res | c << 16, word 3 = t0 | t1 << 16. */
 typedef struct {
     uint8_t op;      /* GEVO_OP_* */
+    uint8_t aux;     /* cmp: predicate (evoir::CmpPred); select / load: tag of the result kind;
+                        getindex: 1 when inst.type is ptr<shared>; br: number of targets;
+                        phi: number of arms */
+    uint8_t otag;    /* arithmetic / compares: tag both operands must carry */
     uint8_t cls;     /* GEVO_COST_* */
-    uint8_t want;    /* load: tag of the loaded kind; select: tag of inst.type;
-                        getindex: 1 when inst.type is ptr<shared>;
-                        cmp: predicate (evoir::CmpPred); br: number of targets */
-    uint8_t flags;   /* reserved */
+    uint16_t a;      /* operand refs */
+    uint16_t b;
     uint16_t res;    /* result slot or GEVO_NO_RESULT */
-    uint16_t a;      /* operand refs; phi: arm offset (relative to variant arm base) */
-    uint16_t b;      /* phi: arm count; sync: barrier id */
-    uint16_t c;
-    int16_t t0;      /* br targets (block index, -1 = unknown label) */
-    int16_t t1;
+    uint16_t c;      /* select: false arm; store: value; phi with > 2 arms: arm offset */
+    int16_t t0;      /* br targets (block index, -1 = unknown label); phi with <= 2 arms: */
+    int16_t t1;      /* predecessor block of arm a / arm b */
 } gevo_inst;
 
 typedef struct {
@@ -174,7 +176,7 @@ typedef struct {
 } gevo_batch_header;
 
 #define GEVO_MAGIC 0x4F564547u
-#define GEVO_VERSION 1u
+#define GEVO_VERSION 2u
 
 /* Per-(variant, test) record written by the interpreter. */
 typedef struct {
@@ -184,7 +186,7 @@ typedef struct {
     int32_t aux;     /* trap payload: slot / param index */
     uint8_t status;  /* GEVO_STATUS_* */
     uint8_t code;    /* GEVO_OK / GEVO_TRAP_* / GEVO_BUDGET_EXCEEDED / GEVO_SKIPPED */
-    uint8_t pad[2];
+    uint8_t pad[2];  /* pad[0]: spin-accelerator jumps taken (diagnostic) */
 } gevo_test_record;
 
 /* Per-variant EvalOutcome (evaluate_fitness, src/vm.cpp:558-579). */

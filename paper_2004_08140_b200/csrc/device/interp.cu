@@ -1,25 +1,53 @@
 // Batched sm_100a interpreter for the evoir SSA IR.
 //
-// One CUDA thread ("lane") executes one (variant, test) instance. Lanes are
-// ordered variant-major, so the lanes of a warp run the same variant on
-// consecutive tests: they fetch the same 16-byte instruction (broadcast), take
-// the same dispatch branch, read/write the same value-file slot (conflict-free
-// [slot][lane] shared-memory layout) and load consecutive words of the
-// test-interleaved input pool (coalesced).
+// Mapping. One warp runs ONE variant: lane t executes test t (tests > 32 use
+// several warps of the same variant), so the warp fetches the same 16-byte
+// instruction (broadcast load), takes the same dispatch branch, reads and
+// writes the same value-file row ([slot][lane] in shared memory, 8-byte
+// {payload, tag} entries, conflict-free) and loads consecutive words of the
+// test-interleaved input pool (coalesced). Different variants never share a
+// warp, so control flow diverges only on data-dependent branches.
 //
-// Inside a lane the simulated threads run exactly as the reference's
-// Machine::run (src/vm.cpp:114-150 of arxiv/paper_2004_08140): one at a time
-// in id order up to the next barrier or ret, then the barrier-divergence check.
-// Per-instruction semantics follow run_to_barrier / enter_block / step
-// (src/vm.cpp:293-482): cost and budget are charged before any effect, phis
-// read all arms before writing (parallel copy), traps carry the reference's
-// reason codes. Floating point is IEEE binary32 round-to-nearest with no FMA
-// contraction (__f*_rn intrinsics, -fmad=false), double for the error metric.
+// Semantics. Inside a lane the simulated threads run exactly as the
+// reference's Machine::run (src/vm.cpp:114-150 of arxiv/paper_2004_08140): one
+// at a time in id order up to the next barrier or ret, then the
+// barrier-divergence check. Per-instruction semantics follow run_to_barrier /
+// enter_block / step (src/vm.cpp:293-482): cost and budget are charged before
+// any effect, phis read all arms before writing (parallel copy), traps carry
+// the reference's reason codes. Floating point is IEEE binary32
+// round-to-nearest with no FMA contraction (__f*_rn, -fmad=false); the error
+// metric is IEEE double.
+//
+// Accounting. Cost, dynamic-IR and the per-thread budget counter are charged
+// a whole block at a time on entry (block costs are precomputed per launch by
+// block_cost_kernel); leaving a block early (trap, sync, ret, a mid-block
+// branch) refunds the instructions that did not run. A block that could
+// cross the budget runs in exact per-instruction mode, so the budget trap
+// fires on the same instruction as in the reference.
+//
+// Spin accelerator (exact). A simulated thread that passes
+// `spin_threshold` executed instructions is probably spinning in a mutated
+// loop until the 10^6-instruction budget (hard part 2). At a
+// loop anchor block the lane snapshots the value file twice (S0, S1) and
+// hypothesises that every I32/pointer slot moves by a constant stride per
+// iteration and everything else is fixed. It then executes one more iteration
+// while tracking strides through each instruction (add/sub/getindex add
+// strides, mul by a constant scales them, compares must provably keep their
+// outcome over every remaining iteration, loads/stores need fixed addresses
+// and stores must not change memory, float/div/select-condition operands
+// must be fixed). If the iterate S2 = S1 + stride and the tracked strides
+// equal the hypothesis, the state sequence is affine with a fixed path until
+// the budget runs out, so the lane jumps n whole iterations (values += n *
+// stride, counters += n * per-iteration counts) and resumes exact
+// interpretation, which then hits the budget trap on the reference's
+// instruction. Any failed check just continues plain interpretation.
 #include "interp.cuh"
 
 #include <cuda_runtime.h>
 
 namespace gevo {
+
+extern __shared__ __align__(16) uint2 g_vfs[]; // value files of the CTA's warps
 
 namespace {
 
@@ -28,33 +56,20 @@ constexpr int kStopRet = 1, kStopSync = 2, kStopTrap = 3;
 constexpr uint32_t kTsFresh = 0, kTsResume = 3u << 16; // never run / resume after barrier
 constexpr uint32_t kTsRet = 1u << 16, kTsSync = 2u << 16;
 
-struct Inst {
-    uint32_t op, cls, want, res, a, b, c;
-    int32_t t0, t1;
-};
+// Field accessors of the 16-byte record (bytecode.h).
+__device__ __forceinline__ uint32_t f_op(const uint4& r) { return r.x & 0xFF; }
+__device__ __forceinline__ uint32_t f_aux(const uint4& r) { return (r.x >> 8) & 0xFF; }
+__device__ __forceinline__ uint32_t f_otag(const uint4& r) { return (r.x >> 16) & 0xFF; }
+__device__ __forceinline__ uint32_t f_cls(const uint4& r) { return r.x >> 24; }
+__device__ __forceinline__ uint32_t f_a(const uint4& r) { return r.y & 0xFFFF; }
+__device__ __forceinline__ uint32_t f_b(const uint4& r) { return r.y >> 16; }
+__device__ __forceinline__ uint32_t f_res(const uint4& r) { return r.z & 0xFFFF; }
+__device__ __forceinline__ uint32_t f_c(const uint4& r) { return r.z >> 16; }
+__device__ __forceinline__ int32_t f_t0(const uint4& r) { return static_cast<int16_t>(r.w & 0xFFFF); }
+__device__ __forceinline__ int32_t f_t1(const uint4& r) { return static_cast<int16_t>(r.w >> 16); }
 
-__device__ __forceinline__ Inst load_inst(const gevo_inst* code, uint32_t idx) {
-    const uint4 r = __ldg(reinterpret_cast<const uint4*>(code) + idx);
-    Inst in;
-    in.op = r.x & 0xFF;
-    in.cls = (r.x >> 8) & 0xFF;
-    in.want = (r.x >> 16) & 0xFF;
-    in.res = r.y & 0xFFFF;
-    in.a = r.y >> 16;
-    in.b = r.z & 0xFFFF;
-    in.c = r.z >> 16;
-    in.t0 = static_cast<int16_t>(r.w & 0xFFFF);
-    in.t1 = static_cast<int16_t>(r.w >> 16);
-    return in;
-}
-
-__device__ __forceinline__ gevo_block load_block(const gevo_block* blk, int b) {
-    const uint2 r = __ldg(reinterpret_cast<const uint2*>(blk) + b);
-    gevo_block g;
-    g.start = r.x;
-    g.len = static_cast<uint16_t>(r.y & 0xFFFF);
-    g.nphi = static_cast<uint16_t>(r.y >> 16);
-    return g;
+__device__ __forceinline__ uint4 fetch_inst(const gevo_inst* code, uint32_t idx) {
+    return __ldg(reinterpret_cast<const uint4*>(code) + idx);
 }
 
 __device__ __forceinline__ bool is_ptr_tag(uint32_t t) {
@@ -89,16 +104,23 @@ __device__ __forceinline__ double word_to_double(uint32_t w, uint32_t elem) {
                                 : static_cast<double>(__uint_as_float(w));
 }
 
+__device__ __forceinline__ bool bad_tag(uint32_t t) {
+    return t == GEVO_TAG_UNDEF || t == GEVO_TAG_POISON_PARAM || t == GEVO_TAG_POISON_MISSING;
+}
+
+// Value file of one lane: slot s lives at index base + s * row of the CTA's
+// shared array (kSmem) or of the global scratch array.
+template <bool kSmem>
 struct Lane {
-    // value file (already offset by lane; slot s at s * stride)
-    uint32_t* pay;
-    uint8_t* tag;
-    int stride;
+    uint2* gvf;      // global value file (when !kSmem)
+    uint32_t base;   // element index of slot 0
+    uint32_t row;
     // program
     const gevo_inst* code;
-    const gevo_block* blk;
+    const uint4* dblk;  // block records of this variant
     const gevo_arm* arm;
     uint32_t n_values;
+    uint32_t n_slots;
     uint32_t stage_base;
     uint64_t writable;
     // instance
@@ -108,56 +130,63 @@ struct Lane {
     int64_t cost;
     int64_t ir;
     int32_t poll;
+    uint32_t jumps;   // spin-accelerator jumps (diagnostic, saturating)
+    uint32_t spin_dbg;// last spin-accelerator abandon reason (diagnostic)
     // trap
     uint32_t code_out;
     int32_t aux;
 
-    __device__ __forceinline__ uint32_t& P(uint32_t s) { return pay[s * stride]; }
-    __device__ __forceinline__ uint8_t& G(uint32_t s) { return tag[s * stride]; }
+    __device__ __forceinline__ uint2 V(uint32_t s) const {
+        if (kSmem)
+            return g_vfs[base + s * row];
+        return gvf[base + s * row];
+    }
+    __device__ __forceinline__ void W(uint32_t s, uint32_t payload, uint32_t tag) {
+        if (kSmem)
+            g_vfs[base + s * row] = make_uint2(payload, tag);
+        else
+            gvf[base + s * row] = make_uint2(payload, tag);
+    }
 
     __device__ __forceinline__ bool trap(uint32_t c, int32_t x = 0) {
         code_out = c;
         aux = x;
         return false;
     }
-
-    // Generic fetch (vm.cpp:195-222): undefined / poisoned slots trap.
-    __device__ __forceinline__ bool fetch(uint32_t s, uint32_t& t, uint32_t& p) {
-        t = G(s);
-        p = P(s);
+    // Trap of a generic fetch (vm.cpp:195-222) for a slot whose tag is t.
+    __device__ __forceinline__ bool fetch_trap(uint32_t s, uint32_t t) {
         if (t == GEVO_TAG_UNDEF)
             return trap(GEVO_TRAP_UNDEF_VALUE, static_cast<int32_t>(s));
         if (t == GEVO_TAG_POISON_PARAM)
             return trap(GEVO_TRAP_BAD_PARAM);
-        if (t == GEVO_TAG_POISON_MISSING)
-            return trap(GEVO_TRAP_BAD_OPERAND);
+        return trap(GEVO_TRAP_BAD_OPERAND);
+    }
+    // fetch (vm.cpp:195-222): undefined / poisoned slots trap.
+    __device__ __forceinline__ bool fetch(uint32_t s, uint2& v) {
+        v = V(s);
+        if (bad_tag(v.y))
+            return fetch_trap(s, v.y);
         return true;
     }
-    // fetch_scalar (vm.cpp:224-229)
-    __device__ __forceinline__ bool scalar(uint32_t s, uint32_t want, uint32_t& p) {
-        const uint32_t t = G(s);
-        p = P(s);
-        if (t == want)
-            return true;
-        uint32_t tt, pp;
-        if (!fetch(s, tt, pp))
-            return false;
+    // fetch_scalar (vm.cpp:224-229) failure: the first failing operand decides.
+    __device__ __forceinline__ bool scalar_fail(uint32_t s, uint32_t t) {
+        if (bad_tag(t))
+            return fetch_trap(s, t);
         return trap(GEVO_TRAP_OPERAND_TYPE);
     }
     // fetch_ptr (vm.cpp:231-236)
-    __device__ __forceinline__ bool pointer(uint32_t s, uint32_t& t, uint32_t& off) {
-        if (!fetch(s, t, off))
+    __device__ __forceinline__ bool pointer(uint32_t s, uint2& v) {
+        if (!fetch(s, v))
             return false;
-        if (!is_ptr_tag(t))
+        if (!is_ptr_tag(v.y))
             return trap(GEVO_TRAP_NOT_POINTER);
         return true;
     }
     // set (vm.cpp:285-291)
-    __device__ __forceinline__ bool set(uint32_t res, uint32_t t, uint32_t p) {
+    __device__ __forceinline__ bool set(uint32_t res, uint32_t payload, uint32_t t) {
         if (res == GEVO_NO_RESULT)
             return trap(GEVO_TRAP_DEF_NO_ID);
-        G(res) = static_cast<uint8_t>(t);
-        P(res) = p;
+        W(res, payload, t);
         return true;
     }
 };
@@ -166,88 +195,709 @@ struct Thread {
     int32_t block, ip, prev;
     int64_t executed;
     uint32_t bar;
+    bool slow; // current block runs with per-instruction charging
 };
 
-__device__ __forceinline__ bool charge(Lane& L, Thread& th, const int64_t* s_cost, uint32_t cls,
-                                       int64_t budget) {
+// Current block of a thread (decoded block record).
+struct Blk {
+    uint32_t start, len, nphi;
+};
+
+__device__ __forceinline__ Blk load_blk(const uint4* dblk, int32_t b, int64_t& cost) {
+    const uint4 r = __ldg(dblk + b);
+    Blk k;
+    k.start = r.x;
+    k.len = r.y & 0xFFFF;
+    k.nphi = r.y >> 16;
+    cost = static_cast<int64_t>((static_cast<uint64_t>(r.w) << 32) | r.z);
+    return k;
+}
+
+// Spin-accelerator state of the running simulated thread.
+struct Spin {
+    uint32_t mode;     // 0 idle, 1 have S0, 2 abstract iterate running
+    int32_t anchor;
+    uint32_t skip;     // block entries to pass before choosing an anchor
+    uint32_t attempts;
+    int64_t next;      // executed count that arms the next attempt
+    int64_t e0, c0;    // executed / lane cost at the reference iterate
+    int64_t p, c;      // per-iteration instructions / cost
+    int64_t H;         // iterations the abstract proof must cover
+    uint32_t nst, nld; // store / load log entries of the abstract iterate
+};
+
+template <bool kSmem>
+__device__ __forceinline__ int64_t suffix_cost(const Lane<kSmem>& L, const Blk& b, uint32_t from,
+                                               const int64_t* s_cost) {
+    int64_t c = 0;
+    for (uint32_t j = from; j < b.len; ++j)
+        c += s_cost[__ldg(reinterpret_cast<const uint32_t*>(L.code + b.start + j)) >> 24];
+    return c;
+}
+
+// Charges instructions [from, len) of the current block on entry / resume.
+template <bool kSmem>
+__device__ __forceinline__ void charge_block(const InterpArgs& A, Lane<kSmem>& L, Thread& th,
+                                             const Blk& b, int64_t bcost, uint32_t from,
+                                             const int64_t* s_cost) {
+    const int64_t n = static_cast<int64_t>(b.len) - from;
+    if (th.executed + n <= A.budget) {
+        L.cost += from == 0 ? bcost : suffix_cost(L, b, from, s_cost);
+        L.ir += n;
+        th.executed += n;
+        th.slow = false;
+    } else {
+        th.slow = true;
+    }
+}
+
+// Refunds instructions [from, len) charged on entry that will not run.
+template <bool kSmem>
+__device__ __forceinline__ void refund(Lane<kSmem>& L, Thread& th, const Blk& b, uint32_t from,
+                                       const int64_t* s_cost) {
+    if (th.slow || from >= b.len)
+        return;
+    const int64_t n = static_cast<int64_t>(b.len) - from;
+    L.cost -= suffix_cost(L, b, from, s_cost);
+    L.ir -= n;
+    th.executed -= n;
+}
+
+// Per-instruction charge (exact mode): cost and budget before any effect.
+template <bool kSmem>
+__device__ __forceinline__ bool charge_one(const InterpArgs& A, Lane<kSmem>& L, Thread& th,
+                                           uint32_t cls, const int64_t* s_cost) {
     L.cost += s_cost[cls];
     ++L.ir;
-    if (++th.executed > budget)
+    if (++th.executed > A.budget)
         return L.trap(GEVO_BUDGET_EXCEEDED);
     return true;
 }
 
+// ---- spin accelerator --------------------------------------------------------
+//
+// Abstract values of the iterate: affine int (stride, 0 = constant) or
+// "varying" (any value; allowed only where it cannot change the path: float
+// arithmetic, phi / select arms, stored values). A budget-bound spinner's
+// record (status, cost, dynamic IR) depends on its path only, so varying
+// values need no extrapolation; everything the path reads (branch and select
+// conditions, compare operands, addresses, divisors, tags) must be affine
+// with a provably constant outcome.
+
+template <bool kSmem>
+__device__ __forceinline__ size_t sp_at(const InterpArgs& A, const Lane<kSmem>& L, uint32_t s) {
+    return static_cast<size_t>(s) * A.n_inst + L.il;
+}
+
+template <bool kSmem>
+__device__ __forceinline__ void spin_abandon(Spin& S, const Thread& th, Lane<kSmem>& L,
+                                             uint32_t why) {
+    S.mode = 0;
+    ++S.attempts;
+    S.skip = S.attempts & 3u;
+    S.next = S.attempts > 12 ? INT64_MAX : th.executed + (th.executed >> 1) + 64;
+    L.spin_dbg = why;
+}
+
+__device__ __forceinline__ bool slot_strided(uint32_t tag) {
+    return tag == GEVO_TAG_I32 || is_ptr_tag(tag);
+}
+
+// Does (X + k*sx) pred (Y + k*sy) keep its k = 0 outcome for all k in [0, H]
+// with neither side leaving the int32 range?
+__device__ bool cmp_constant(int32_t X, int32_t sx, int32_t Y, int32_t sy, uint32_t pred,
+                             int64_t H) {
+    const int64_t xH = static_cast<int64_t>(X) + H * sx;
+    const int64_t yH = static_cast<int64_t>(Y) + H * sy;
+    if (xH < INT32_MIN || xH > INT32_MAX || yH < INT32_MIN || yH > INT32_MAX)
+        return false;
+    const int64_t f0 = static_cast<int64_t>(X) - Y;
+    const int64_t slope = static_cast<int64_t>(sx) - sy;
+    if (slope == 0)
+        return true;
+    if (pred <= 1) { // eq / ne: no root of f in [0, H]
+        if (f0 % slope != 0)
+            return true;
+        const int64_t r = -f0 / slope;
+        return r < 0 || r > H;
+    }
+    return cmp(static_cast<int64_t>(X), static_cast<int64_t>(Y), pred) == cmp(xH, yH, pred);
+}
+
+template <bool kSmem>
+__device__ __forceinline__ uint32_t spin_stride(const InterpArgs& A, const Lane<kSmem>& L,
+                                                uint32_t s) {
+    return s < L.n_slots ? A.sp_cur[sp_at(A, L, s)] : 0u;
+}
+template <bool kSmem>
+__device__ __forceinline__ uint32_t spin_vary(const InterpArgs& A, const Lane<kSmem>& L,
+                                              uint32_t s) {
+    return s < L.n_slots ? A.sp_cvary[sp_at(A, L, s)] : 0u;
+}
+template <bool kSmem>
+__device__ __forceinline__ void spin_set(const InterpArgs& A, const Lane<kSmem>& L, uint32_t s,
+                                         uint32_t stride, uint32_t vary) {
+    if (s < L.n_slots) {
+        A.sp_cur[sp_at(A, L, s)] = stride;
+        A.sp_cvary[sp_at(A, L, s)] = static_cast<uint8_t>(vary);
+    }
+}
+
+// Memory word key of a store / load of the iterate (0: not representable).
+__device__ __forceinline__ uint32_t mem_key(uint32_t ptag, int64_t eff) {
+    if (eff < 0 || eff >= (1 << 24))
+        return 0;
+    const uint32_t space = ptag == GEVO_TAG_PTR_SHARED ? 0x80u : ((ptag & 0x3F) + 1);
+    return (space << 24) | static_cast<uint32_t>(eff);
+}
+
+template <bool kSmem>
+__device__ __forceinline__ size_t log_at(const InterpArgs& A, const Lane<kSmem>& L, uint32_t i,
+                                         uint32_t field) {
+    return (static_cast<size_t>(field) * kSpinLog + i) * A.n_inst + L.il;
+}
+
+// Current memory word (payload, tag) behind a key.
+template <bool kSmem>
+__device__ __forceinline__ uint2 mem_word(const InterpArgs& A, const Lane<kSmem>& L, uint32_t key) {
+    const uint32_t eff = key & 0xFFFFFF, space = key >> 24;
+    if (space == 0x80) {
+        const size_t at = static_cast<size_t>(eff) * A.n_inst + L.il;
+        return make_uint2(A.sh_val[at], A.sh_tag[at]);
+    }
+    const uint32_t prm = space - 1;
+    return make_uint2(A.priv[A.priv_off[prm] + static_cast<size_t>(eff) * A.n_inst + L.il], 0);
+}
+
+// Stride transfer of one instruction of the abstract iterate, called before
+// its concrete execution (operands still hold their k = 0 values). Returns
+// false when the instruction breaks the proof.
+template <bool kSmem>
+__device__ __forceinline__ bool spin_track(const InterpArgs& A, const Lane<kSmem>& L,
+                                           const uint4 r, Spin& S) {
+    const uint32_t op = f_op(r), a = f_a(r), b = f_b(r), c = f_c(r), res = f_res(r);
+    uint32_t out = 0, vout = 0;
+    const uint32_t sa = spin_stride(A, L, a), sb = spin_stride(A, L, b);
+    const uint32_t va = spin_vary(A, L, a), vb = spin_vary(A, L, b);
+    switch (op) {
+    case GEVO_OP_ADD: out = sa + sb; vout = va | vb; break;
+    case GEVO_OP_SUB: out = sa - sb; vout = va | vb; break;
+    case GEVO_OP_GETINDEX: out = sa + sb; vout = va | vb; break;
+    case GEVO_OP_MUL:
+        vout = va | vb;
+        if (!vout) {
+            if (sa && sb)
+                vout = 1;
+            else
+                out = sa ? sa * L.V(b).x : sb * L.V(a).x;
+        }
+        break;
+    case GEVO_OP_SDIV: // may trap: operands must be fixed
+        if (sa | sb | va | vb)
+            return false;
+        break;
+    case GEVO_OP_FADD: case GEVO_OP_FSUB: case GEVO_OP_FMUL: case GEVO_OP_FDIV:
+    case GEVO_OP_FCMP:
+        vout = (sa | sb | va | vb) ? 1u : 0u;
+        break;
+    case GEVO_OP_ICMP:
+        if (va | vb) {
+            vout = 1;
+        } else if (sa | sb) {
+            const uint2 x = L.V(a), y = L.V(b);
+            if (x.y != GEVO_TAG_I32 || y.y != GEVO_TAG_I32)
+                return false;
+            if (!cmp_constant(static_cast<int32_t>(x.x), static_cast<int32_t>(sa),
+                              static_cast<int32_t>(y.x), static_cast<int32_t>(sb), f_aux(r), S.H))
+                return false;
+        }
+        break;
+    case GEVO_OP_SELECT: {
+        if (sa | va)
+            return false;
+        const uint32_t arm = L.V(a).x ? b : c;
+        out = spin_stride(A, L, arm);
+        vout = spin_vary(A, L, arm);
+        break;
+    }
+    case GEVO_OP_LOAD: case GEVO_OP_STORE: {
+        if (sa | sb | va | vb)
+            return false;
+        const uint2 p = L.V(a), i = L.V(b);
+        if (!is_ptr_tag(p.y) || i.y != GEVO_TAG_I32)
+            return false;
+        const int64_t eff = static_cast<int64_t>(static_cast<int32_t>(p.x)) +
+                            static_cast<int32_t>(i.x);
+        if (p.y == GEVO_TAG_PTR_SHARED) {
+            if (eff < 0 || eff >= A.shared_words)
+                return false;
+        } else {
+            const uint32_t prm = p.y & 0x3F;
+            const int32_t size = __ldg(A.buf_size + static_cast<size_t>(L.t) * A.n_params + prm);
+            if (eff < 0 || eff >= size)
+                return false;
+            if (!((L.writable >> prm) & 1ull)) {
+                if (op == GEVO_OP_STORE)
+                    return false;
+                break; // read-only pool word: constant
+            }
+        }
+        const uint32_t key = mem_key(p.y, eff);
+        if (!key)
+            return false;
+        uint32_t hit = kSpinLog;
+        for (uint32_t j = 0; j < S.nst; ++j)
+            if (A.sp_log[log_at(A, L, j, 0)] == key)
+                hit = j;
+        if (op == GEVO_OP_LOAD) {
+            if (hit < kSpinLog && (A.sp_log[log_at(A, L, hit, 2)] & 0x100)) {
+                vout = 1;
+            } else {
+                if (S.nld >= kSpinLog)
+                    return false;
+                A.sp_ld[log_at(A, L, S.nld++, 0)] = key;
+            }
+            break;
+        }
+        const uint32_t vary_store = (spin_stride(A, L, c) | spin_vary(A, L, c)) ? 0x100u : 0u;
+        if (hit == kSpinLog) {
+            if (S.nst >= kSpinLog)
+                return false;
+            const uint2 old = mem_word(A, L, key);
+            A.sp_log[log_at(A, L, S.nst, 0)] = key;
+            A.sp_log[log_at(A, L, S.nst, 1)] = old.x;
+            A.sp_log[log_at(A, L, S.nst, 2)] = old.y | vary_store;
+            ++S.nst;
+        } else {
+            A.sp_log[log_at(A, L, hit, 2)] |= vary_store;
+        }
+        return true;
+    }
+    case GEVO_OP_BR:
+        return !(f_aux(r) == 2 && (sa | va));
+    case GEVO_OP_CONST: out = sa; vout = va; break;
+    default: break; // tid / nthreads / sync / ret: fixed or no result
+    }
+    if (res != GEVO_NO_RESULT)
+        spin_set(A, L, res, vout ? 0u : out, vout);
+    return true;
+}
+
+// Protocol step at every completed block entry (phis done).
+template <bool kSmem>
+__device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kSmem>& L, Thread& th,
+                                              Spin& S) {
+    if (S.mode == 0) {
+        if (th.executed < S.next)
+            return;
+        if (S.skip) {
+            --S.skip;
+            return;
+        }
+        for (uint32_t x = 0; x < L.n_values; ++x) {
+            const uint2 v = L.V(x);
+            A.sp_base[sp_at(A, L, x)] = v.x;
+            A.sp_btag[sp_at(A, L, x)] = static_cast<uint8_t>(v.y);
+        }
+        S.anchor = th.block;
+        S.e0 = th.executed;
+        S.c0 = L.cost;
+        S.mode = 1;
+        return;
+    }
+    if (th.block != S.anchor)
+        return;
+    if (S.mode == 1) {
+        // S1: stride hypothesis from S1 - S0 (non-int changes: varying)
+        const int64_t p = th.executed - S.e0;
+        if (p <= 0) {
+            spin_abandon(S, th, L, 1);
+            return;
+        }
+        for (uint32_t x = 0; x < L.n_values; ++x) {
+            const uint2 v = L.V(x);
+            const size_t at = sp_at(A, L, x);
+            if (A.sp_btag[at] != v.y) {
+                spin_abandon(S, th, L, 2);
+                return;
+            }
+            uint32_t d = v.x - A.sp_base[at];
+            uint8_t vary = 0;
+            if (d && !slot_strided(v.y)) {
+                vary = 1;
+                d = 0;
+            }
+            A.sp_delta[at] = d;
+            A.sp_base[at] = v.x;
+            A.sp_cur[at] = d;
+            A.sp_hvary[at] = vary;
+            A.sp_cvary[at] = vary;
+        }
+        for (uint32_t x = L.n_values; x < L.n_slots; ++x) {
+            A.sp_cur[sp_at(A, L, x)] = 0;
+            A.sp_cvary[sp_at(A, L, x)] = 0;
+        }
+        S.p = p;
+        S.c = L.cost - S.c0;
+        S.e0 = th.executed;
+        S.c0 = L.cost;
+        S.nst = 0;
+        S.nld = 0;
+        S.H = (A.budget - th.executed) / p;
+        if (S.H < 3) {
+            spin_abandon(S, th, L, 4);
+            return;
+        }
+        S.mode = 2;
+        return;
+    }
+    // mode 2: the abstract iterate arrived back at the anchor (S2).
+    if (th.executed - S.e0 != S.p || L.cost - S.c0 != S.c) {
+        spin_abandon(S, th, L, 5);
+        return;
+    }
+    for (uint32_t x = 0; x < L.n_values; ++x) {
+        const uint2 v = L.V(x);
+        const size_t at = sp_at(A, L, x);
+        bool ok = A.sp_btag[at] == v.y;
+        if (ok && !A.sp_hvary[at])
+            ok = !A.sp_cvary[at] && v.x - A.sp_base[at] == A.sp_delta[at] &&
+                 A.sp_cur[at] == A.sp_delta[at];
+        if (!ok) {
+            spin_abandon(S, th, L, 6);
+            return;
+        }
+    }
+    // memory: fixed-value words are back to their S1 contents; no fixed load
+    // reads a word that holds varying data
+    for (uint32_t j = 0; j < S.nst; ++j) {
+        const uint32_t key = A.sp_log[log_at(A, L, j, 0)];
+        const uint32_t tf = A.sp_log[log_at(A, L, j, 2)];
+        if (tf & 0x100) {
+            for (uint32_t k = 0; k < S.nld; ++k)
+                if (A.sp_ld[log_at(A, L, k, 0)] == key) {
+                    spin_abandon(S, th, L, 7);
+                    return;
+                }
+            continue;
+        }
+        const uint2 now = mem_word(A, L, key);
+        if (now.x != A.sp_log[log_at(A, L, j, 1)] || now.y != (tf & 0xFF)) {
+            spin_abandon(S, th, L, 8);
+            return;
+        }
+    }
+    const int64_t n = (A.budget - th.executed) / S.p;
+    if (n > 0) {
+        for (uint32_t x = 0; x < L.n_values; ++x) {
+            const size_t at = sp_at(A, L, x);
+            const uint32_t d = A.sp_delta[at];
+            if (d && !A.sp_hvary[at]) {
+                const uint2 v = L.V(x);
+                L.W(x, v.x + static_cast<uint32_t>(n) * d, v.y);
+            }
+        }
+        th.executed += n * S.p;
+        L.ir += n * S.p;
+        L.cost += n * S.c;
+        L.jumps = min(L.jumps + 1u, 255u);
+        if (A.counters) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(A.counters), 1ull);
+            atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 1),
+                      static_cast<unsigned long long>(n * S.p));
+        }
+    }
+    S.mode = 0;
+    S.next = INT64_MAX;
+}
+
+// Phi arm for predecessor `prev` (first matching arm, vm.cpp:311-323);
+// returns false when no arm matches.
+template <bool kSmem>
+__device__ __forceinline__ bool phi_arm(const Lane<kSmem>& L, const uint4 r, int32_t prev,
+                                        uint32_t& ref) {
+    const uint32_t n = f_aux(r);
+    if (n <= 2) {
+        if (n >= 1 && f_t0(r) == prev) {
+            ref = f_a(r);
+            return true;
+        }
+        if (n == 2 && f_t1(r) == prev) {
+            ref = f_b(r);
+            return true;
+        }
+        return false;
+    }
+    const uint32_t* arms = reinterpret_cast<const uint32_t*>(L.arm) + f_c(r);
+    for (uint32_t a = 0; a < n; ++a) {
+        const uint32_t raw = __ldg(arms + a);
+        if (static_cast<int16_t>(raw & 0xFFFF) == prev) {
+            ref = raw >> 16;
+            return true;
+        }
+    }
+    return false;
+}
+
 // enter_block (vm.cpp:293-333): charge and stage every leading phi, then write.
-__device__ bool enter_block(const InterpArgs& A, Lane& L, Thread& th, const int64_t* s_cost,
-                            int target, gevo_block& b) {
+template <bool kSmem>
+__device__ bool enter_block(const InterpArgs& A, Lane<kSmem>& L, Thread& th, const int64_t* s_cost,
+                            int32_t target, Blk& b, Spin& S) {
     th.prev = th.block;
     th.block = target;
     th.ip = 0;
-    b = load_block(L.blk, target);
+    int64_t bcost;
+    b = load_blk(L.dblk, target, bcost);
+    charge_block(A, L, th, b, bcost, 0, s_cost);
     const uint32_t n = b.nphi;
-    for (uint32_t j = 0; j < n; ++j) {
-        const Inst phi = load_inst(L.code, b.start + j);
-        if (!charge(L, th, s_cost, phi.cls, A.budget))
+    if (n == 0)
+        return true;
+    const bool track = S.mode == 2;
+    if (n == 1) {
+        // a single phi reads nothing another phi writes: no staging needed
+        const uint4 r = fetch_inst(L.code, b.start);
+        if (th.slow && !charge_one(A, L, th, f_cls(r), s_cost))
             return false;
-        bool matched = false;
-        for (uint32_t a = 0; a < phi.b; ++a) {
-            const uint32_t raw = __ldg(reinterpret_cast<const uint32_t*>(L.arm) + phi.a + a);
-            const int32_t from = static_cast<int16_t>(raw & 0xFFFF);
-            if (from != th.prev)
-                continue;
-            uint32_t t, p;
-            if (!L.fetch(raw >> 16, t, p))
-                return false;
-            L.G(L.stage_base + j) = static_cast<uint8_t>(t);
-            L.P(L.stage_base + j) = p;
-            matched = true;
-            break;
-        }
-        if (!matched)
+        uint32_t ref;
+        if (!phi_arm(L, r, th.prev, ref)) {
+            refund(L, th, b, 1, s_cost);
             return L.trap(GEVO_TRAP_PHI_NO_INCOMING);
+        }
+        uint2 v;
+        if (!L.fetch(ref, v)) {
+            refund(L, th, b, 1, s_cost);
+            return false;
+        }
+        th.ip = 1;
+        if (!L.set(f_res(r), v.x, v.y)) {
+            refund(L, th, b, 1, s_cost);
+            return false;
+        }
+        if (track)
+            spin_set(A, L, f_res(r), spin_stride(A, L, ref), spin_vary(A, L, ref));
+        return true;
+    }
+    for (uint32_t j = 0; j < n; ++j) {
+        const uint4 r = fetch_inst(L.code, b.start + j);
+        if (th.slow && !charge_one(A, L, th, f_cls(r), s_cost))
+            return false;
+        uint32_t ref;
+        if (!phi_arm(L, r, th.prev, ref)) {
+            refund(L, th, b, j + 1, s_cost);
+            return L.trap(GEVO_TRAP_PHI_NO_INCOMING);
+        }
+        uint2 v;
+        if (!L.fetch(ref, v)) {
+            refund(L, th, b, j + 1, s_cost);
+            return false;
+        }
+        L.W(L.stage_base + j, v.x, v.y);
+        if (track)
+            spin_set(A, L, L.stage_base + j, spin_stride(A, L, ref), spin_vary(A, L, ref));
         ++th.ip;
     }
     for (uint32_t j = 0; j < n; ++j) {
-        const Inst phi = load_inst(L.code, b.start + j);
-        if (!L.set(phi.res, L.G(L.stage_base + j), L.P(L.stage_base + j)))
+        const uint4 r = fetch_inst(L.code, b.start + j);
+        const uint2 v = L.V(L.stage_base + j);
+        if (!L.set(f_res(r), v.x, v.y)) {
+            refund(L, th, b, n, s_cost);
             return false;
+        }
+        if (track)
+            spin_set(A, L, f_res(r), spin_stride(A, L, L.stage_base + j),
+                     spin_vary(A, L, L.stage_base + j));
     }
     return true;
 }
 
-// run_to_barrier (vm.cpp:340-387) + step (389-482). Returns kStopRet,
-// kStopSync or kStopTrap (L.code_out set).
-__device__ int run_thread(const InterpArgs& A, Lane& L, Thread& th, const int64_t* s_cost,
+// Memory instructions (vm.cpp:238-283, 447-460): off the hot dispatch path.
+template <bool kSmem>
+__device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kSmem>& L, const uint4 r) {
+    const uint32_t op = f_op(r);
+    uint2 p;
+    if (!L.pointer(f_a(r), p))
+        return false;
+    const uint2 ix = L.V(f_b(r));
+    if (ix.y != GEVO_TAG_I32)
+        return L.scalar_fail(f_b(r), ix.y);
+    uint2 val = make_uint2(0, 0);
+    if (op == GEVO_OP_STORE) {
+        if (!L.fetch(f_c(r), val))
+            return false;
+        if (val.y < GEVO_TAG_I32 || val.y > GEVO_TAG_BOOL)
+            return L.trap(GEVO_TRAP_STORE_NONSCALAR);
+        if (val.y == GEVO_TAG_BOOL)
+            return L.trap(GEVO_TRAP_STORE_BOOL);
+    }
+    const int64_t eff = static_cast<int64_t>(static_cast<int32_t>(p.x)) +
+                        static_cast<int64_t>(static_cast<int32_t>(ix.x));
+    if (p.y == GEVO_TAG_PTR_SHARED) {
+        if (eff < 0 || eff >= A.shared_words)
+            return L.trap(GEVO_TRAP_SHARED_OOB);
+        const size_t at = static_cast<size_t>(eff) * A.n_inst + L.il;
+        if (op == GEVO_OP_LOAD) {
+            const uint32_t wt = A.sh_tag[at];
+            if (wt == GEVO_TAG_UNDEF)
+                return L.trap(GEVO_TRAP_SHARED_UNINIT);
+            if (wt != f_aux(r))
+                return L.trap(GEVO_TRAP_SHARED_TYPE);
+            return L.set(f_res(r), A.sh_val[at], wt);
+        }
+        A.sh_tag[at] = static_cast<uint8_t>(val.y);
+        A.sh_val[at] = val.x;
+        return true;
+    }
+    const uint32_t prm = p.y & 0x3F;
+    const size_t tp = static_cast<size_t>(L.t) * A.n_params + prm;
+    const int32_t size = __ldg(A.buf_size + tp);
+    if (eff < 0 || eff >= size)
+        return L.trap(GEVO_TRAP_GLOBAL_OOB);
+    const uint32_t elem = __ldg(A.buf_elem + tp);
+    const bool priv = (L.writable >> prm) & 1ull;
+    if (op == GEVO_OP_LOAD) {
+        if (elem != f_aux(r))
+            return L.trap(GEVO_TRAP_GLOBAL_LOAD_TYPE);
+        const uint32_t w =
+            priv ? A.priv[A.priv_off[prm] + static_cast<size_t>(eff) * A.n_inst + L.il]
+                 : __ldg(A.pool + A.pool_off[prm] + static_cast<size_t>(eff) * A.n_tests + L.t);
+        return L.set(f_res(r), w, elem);
+    }
+    if (elem != val.y)
+        return L.trap(GEVO_TRAP_GLOBAL_STORE_TYPE);
+    if (!priv)
+        return L.trap(GEVO_TRAP_INTERNAL);
+    A.priv[A.priv_off[prm] + static_cast<size_t>(eff) * A.n_inst + L.il] = val.x;
+    return true;
+}
+
+// Non-arithmetic straight-line instructions (select, getindex, intrinsics, const).
+template <bool kSmem>
+__device__ __forceinline__ bool misc_op(const InterpArgs& A, Lane<kSmem>& L, const uint4 r) {
+    switch (f_op(r)) {
+    case GEVO_OP_SELECT: {
+        const uint2 c = L.V(f_a(r));
+        if (c.y != GEVO_TAG_BOOL)
+            return L.scalar_fail(f_a(r), c.y);
+        uint2 v;
+        if (!L.fetch(c.x ? f_b(r) : f_c(r), v))
+            return false;
+        if (v.y != f_aux(r))
+            return L.trap(GEVO_TRAP_SELECT_ARM);
+        return L.set(f_res(r), v.x, v.y);
+    }
+    case GEVO_OP_GETINDEX: {
+        uint2 p;
+        if (!L.pointer(f_a(r), p))
+            return false;
+        if ((p.y == GEVO_TAG_PTR_SHARED ? 1u : 0u) != f_aux(r))
+            return L.trap(GEVO_TRAP_GETINDEX_SPACE);
+        const uint2 ix = L.V(f_b(r));
+        if (ix.y != GEVO_TAG_I32)
+            return L.scalar_fail(f_b(r), ix.y);
+        return L.set(f_res(r), p.x + ix.x, p.y);
+    }
+    case GEVO_OP_TID:
+        return L.set(f_res(r), static_cast<uint32_t>(L.tid), GEVO_TAG_I32);
+    case GEVO_OP_NTHREADS:
+        return L.set(f_res(r), static_cast<uint32_t>(A.threads), GEVO_TAG_I32);
+    case GEVO_OP_CONST: {
+        const uint2 v = L.V(f_a(r));
+        return L.set(f_res(r), v.x, v.y);
+    }
+    default:
+        return L.trap(GEVO_TRAP_UNEXPECTED_OP);
+    }
+}
+
+// run_to_barrier (vm.cpp:340-387) + step (389-482) for one simulated thread
+// from (th.block, th.ip). Returns kStopRet, kStopSync or kStopTrap.
+template <bool kSmem>
+__device__ int run_thread(const InterpArgs& A, Lane<kSmem>& L, Thread& th, const int64_t* s_cost,
                           const volatile int32_t* first_fail) {
-    gevo_block b = load_block(L.blk, th.block);
+    Spin S;
+    S.mode = 0;
+    S.skip = 0;
+    S.attempts = 0;
+    S.next = A.sp_base ? A.spin_threshold : INT64_MAX;
+    int64_t bcost;
+    Blk b = load_blk(L.dblk, th.block, bcost);
+    charge_block(A, L, th, b, bcost, static_cast<uint32_t>(th.ip), s_cost);
+    uint4 nxt = fetch_inst(L.code, b.start + static_cast<uint32_t>(th.ip));
     for (;;) {
-        if (th.ip >= static_cast<int32_t>(b.len)) {
+        const uint32_t ip = static_cast<uint32_t>(th.ip);
+        if (ip >= b.len) {
             L.trap(GEVO_TRAP_FELL_OFF);
             return kStopTrap;
         }
-        const Inst in = load_inst(L.code, b.start + static_cast<uint32_t>(th.ip));
-        if (in.op == GEVO_OP_PHI) {
+        const uint4 r = nxt;
+        // prefetch the next record of the block (the batch array is padded)
+        nxt = fetch_inst(L.code, b.start + ip + 1);
+        const uint32_t op = f_op(r);
+        if (op == GEVO_OP_PHI) {
+            refund(L, th, b, ip, s_cost);
             L.trap(GEVO_TRAP_PHI_OUTSIDE);
             return kStopTrap;
         }
-        if (!charge(L, th, s_cost, in.cls, A.budget))
+        if (th.slow && !charge_one(A, L, th, f_cls(r), s_cost))
             return kStopTrap;
+        if (S.mode == 2 && !spin_track(A, L, r, S))
+            spin_abandon(S, th, L, 0x80 | op);
 
-        bool ok = true;
-        switch (in.op) {
-        case GEVO_OP_SYNC:
-            th.bar = in.b;
-            return kStopSync;
-        case GEVO_OP_RET:
-            return kStopRet;
-        case GEVO_OP_BR: {
-            int target = in.t0;
-            if (in.want == 2) {
-                uint32_t c;
-                if (!L.scalar(in.a, GEVO_TAG_BOOL, c))
-                    return kStopTrap;
-                target = c ? in.t0 : in.t1;
+        bool ok;
+        if (op <= GEVO_OP_FCMP) {
+            // i32 / f32 arithmetic and compares: both operands carry otag
+            const uint2 x = L.V(f_a(r)), y = L.V(f_b(r));
+            const uint32_t otag = f_otag(r);
+            if (x.y != otag) {
+                ok = L.scalar_fail(f_a(r), x.y);
+            } else if (y.y != otag) {
+                ok = L.scalar_fail(f_b(r), y.y);
+            } else {
+                uint32_t v;
+                uint32_t vt = otag;
+                ok = true;
+                const float fx = __uint_as_float(x.x), fy = __uint_as_float(y.x);
+                switch (op) {
+                case GEVO_OP_ADD: v = x.x + y.x; break;
+                case GEVO_OP_SUB: v = x.x - y.x; break;
+                case GEVO_OP_MUL: v = x.x * y.x; break;
+                case GEVO_OP_SDIV: {
+                    const int32_t sx = static_cast<int32_t>(x.x), sy = static_cast<int32_t>(y.x);
+                    if (sy == 0)
+                        ok = L.trap(GEVO_TRAP_DIV_ZERO);
+                    else if (sx == INT32_MIN && sy == -1)
+                        ok = L.trap(GEVO_TRAP_DIV_OVERFLOW);
+                    v = ok ? static_cast<uint32_t>(sx / sy) : 0u;
+                    break;
+                }
+                case GEVO_OP_FADD: v = __float_as_uint(__fadd_rn(fx, fy)); break;
+                case GEVO_OP_FSUB: v = __float_as_uint(__fsub_rn(fx, fy)); break;
+                case GEVO_OP_FMUL: v = __float_as_uint(__fmul_rn(fx, fy)); break;
+                case GEVO_OP_FDIV: v = __float_as_uint(__fdiv_rn(fx, fy)); break;
+                case GEVO_OP_ICMP:
+                    v = cmp(static_cast<int32_t>(x.x), static_cast<int32_t>(y.x), f_aux(r)) ? 1u : 0u;
+                    vt = GEVO_TAG_BOOL;
+                    break;
+                default: // FCMP
+                    v = cmp(fx, fy, f_aux(r)) ? 1u : 0u;
+                    vt = GEVO_TAG_BOOL;
+                    break;
+                }
+                if (ok)
+                    ok = L.set(f_res(r), v, vt);
             }
+        } else if (op == GEVO_OP_BR) {
+            int32_t target = f_t0(r);
+            if (f_aux(r) == 2) {
+                const uint2 c = L.V(f_a(r));
+                if (c.y != GEVO_TAG_BOOL) {
+                    L.scalar_fail(f_a(r), c.y);
+                    refund(L, th, b, ip + 1, s_cost);
+                    return kStopTrap;
+                }
+                target = c.x ? f_t0(r) : f_t1(r);
+            }
+            refund(L, th, b, ip + 1, s_cost);
             if (target < 0) {
                 L.trap(GEVO_TRAP_UNKNOWN_BLOCK);
                 return kStopTrap;
@@ -259,223 +909,47 @@ __device__ int run_thread(const InterpArgs& A, Lane& L, Thread& th, const int64_
                     return kStopTrap;
                 }
             }
-            if (!enter_block(A, L, th, s_cost, target, b))
+            if (!enter_block(A, L, th, s_cost, target, b, S))
                 return kStopTrap;
+            if ((th.executed >= S.next || S.mode != 0) && !th.slow)
+                spin_at_entry(A, L, th, S);
+            nxt = fetch_inst(L.code, b.start + static_cast<uint32_t>(th.ip));
             continue;
+        } else if (op == GEVO_OP_LOAD || op == GEVO_OP_STORE) {
+            ok = mem_op(A, L, r);
+        } else if (op == GEVO_OP_SYNC) {
+            refund(L, th, b, ip + 1, s_cost);
+            th.bar = f_b(r);
+            return kStopSync;
+        } else if (op == GEVO_OP_RET) {
+            refund(L, th, b, ip + 1, s_cost);
+            return kStopRet;
+        } else {
+            ok = misc_op(A, L, r);
         }
-        case GEVO_OP_ADD: case GEVO_OP_SUB: case GEVO_OP_MUL: case GEVO_OP_SDIV: {
-            uint32_t x, y;
-            if (!L.scalar(in.a, GEVO_TAG_I32, x) || !L.scalar(in.b, GEVO_TAG_I32, y))
-                return kStopTrap;
-            uint32_t r;
-            if (in.op == GEVO_OP_ADD) {
-                r = x + y;
-            } else if (in.op == GEVO_OP_SUB) {
-                r = x - y;
-            } else if (in.op == GEVO_OP_MUL) {
-                r = x * y;
-            } else {
-                const int32_t sx = static_cast<int32_t>(x), sy = static_cast<int32_t>(y);
-                if (sy == 0) {
-                    L.trap(GEVO_TRAP_DIV_ZERO);
-                    return kStopTrap;
-                }
-                if (sx == INT32_MIN && sy == -1) {
-                    L.trap(GEVO_TRAP_DIV_OVERFLOW);
-                    return kStopTrap;
-                }
-                r = static_cast<uint32_t>(sx / sy);
-            }
-            ok = L.set(in.res, GEVO_TAG_I32, r);
-            break;
-        }
-        case GEVO_OP_FADD: case GEVO_OP_FSUB: case GEVO_OP_FMUL: case GEVO_OP_FDIV: {
-            uint32_t x, y;
-            if (!L.scalar(in.a, GEVO_TAG_F32, x) || !L.scalar(in.b, GEVO_TAG_F32, y))
-                return kStopTrap;
-            const float fx = __uint_as_float(x), fy = __uint_as_float(y);
-            float r;
-            if (in.op == GEVO_OP_FADD)
-                r = __fadd_rn(fx, fy);
-            else if (in.op == GEVO_OP_FSUB)
-                r = __fsub_rn(fx, fy);
-            else if (in.op == GEVO_OP_FMUL)
-                r = __fmul_rn(fx, fy);
-            else
-                r = __fdiv_rn(fx, fy);
-            ok = L.set(in.res, GEVO_TAG_F32, __float_as_uint(r));
-            break;
-        }
-        case GEVO_OP_ICMP: {
-            uint32_t x, y;
-            if (!L.scalar(in.a, GEVO_TAG_I32, x) || !L.scalar(in.b, GEVO_TAG_I32, y))
-                return kStopTrap;
-            ok = L.set(in.res, GEVO_TAG_BOOL,
-                       cmp(static_cast<int32_t>(x), static_cast<int32_t>(y), in.want) ? 1u : 0u);
-            break;
-        }
-        case GEVO_OP_FCMP: {
-            uint32_t x, y;
-            if (!L.scalar(in.a, GEVO_TAG_F32, x) || !L.scalar(in.b, GEVO_TAG_F32, y))
-                return kStopTrap;
-            ok = L.set(in.res, GEVO_TAG_BOOL,
-                       cmp(__uint_as_float(x), __uint_as_float(y), in.want) ? 1u : 0u);
-            break;
-        }
-        case GEVO_OP_SELECT: {
-            uint32_t c, t, p;
-            if (!L.scalar(in.a, GEVO_TAG_BOOL, c) || !L.fetch(c ? in.b : in.c, t, p))
-                return kStopTrap;
-            if (t != in.want) {
-                L.trap(GEVO_TRAP_SELECT_ARM);
-                return kStopTrap;
-            }
-            ok = L.set(in.res, t, p);
-            break;
-        }
-        case GEVO_OP_LOAD: case GEVO_OP_STORE: {
-            uint32_t pt, off, idx;
-            if (!L.pointer(in.a, pt, off) || !L.scalar(in.b, GEVO_TAG_I32, idx))
-                return kStopTrap;
-            uint32_t vt = 0, vp = 0;
-            if (in.op == GEVO_OP_STORE) {
-                if (!L.fetch(in.c, vt, vp))
-                    return kStopTrap;
-                if (vt < GEVO_TAG_I32 || vt > GEVO_TAG_BOOL) {
-                    L.trap(GEVO_TRAP_STORE_NONSCALAR);
-                    return kStopTrap;
-                }
-                if (vt == GEVO_TAG_BOOL) {
-                    L.trap(GEVO_TRAP_STORE_BOOL);
-                    return kStopTrap;
-                }
-            }
-            const int64_t eff = static_cast<int64_t>(static_cast<int32_t>(off)) +
-                                static_cast<int64_t>(static_cast<int32_t>(idx));
-            const uint32_t nt = static_cast<uint32_t>(A.n_tests);
-            if (pt == GEVO_TAG_PTR_SHARED) {
-                if (eff < 0 || eff >= A.shared_words) {
-                    L.trap(GEVO_TRAP_SHARED_OOB);
-                    return kStopTrap;
-                }
-                const size_t at = static_cast<size_t>(eff) * A.n_inst + L.il;
-                if (in.op == GEVO_OP_LOAD) {
-                    const uint32_t wt = A.sh_tag[at];
-                    if (wt == GEVO_TAG_UNDEF) {
-                        L.trap(GEVO_TRAP_SHARED_UNINIT);
-                        return kStopTrap;
-                    }
-                    if (wt != in.want) {
-                        L.trap(GEVO_TRAP_SHARED_TYPE);
-                        return kStopTrap;
-                    }
-                    ok = L.set(in.res, wt, A.sh_val[at]);
-                } else {
-                    A.sh_tag[at] = static_cast<uint8_t>(vt);
-                    A.sh_val[at] = vp;
-                }
-                break;
-            }
-            const uint32_t p = pt & 0x3F;
-            const size_t tp = static_cast<size_t>(L.t) * A.n_params + p;
-            const int32_t size = __ldg(A.buf_size + tp);
-            if (eff < 0 || eff >= size) {
-                L.trap(GEVO_TRAP_GLOBAL_OOB);
-                return kStopTrap;
-            }
-            const uint32_t elem = __ldg(A.buf_elem + tp);
-            const bool priv = (L.writable >> p) & 1ull;
-            if (in.op == GEVO_OP_LOAD) {
-                if (elem != in.want) {
-                    L.trap(GEVO_TRAP_GLOBAL_LOAD_TYPE);
-                    return kStopTrap;
-                }
-                const uint32_t w =
-                    priv ? A.priv[A.priv_off[p] + static_cast<size_t>(eff) * A.n_inst + L.il]
-                         : __ldg(A.pool + A.pool_off[p] + static_cast<size_t>(eff) * nt + L.t);
-                ok = L.set(in.res, elem, w);
-            } else {
-                if (elem != vt) {
-                    L.trap(GEVO_TRAP_GLOBAL_STORE_TYPE);
-                    return kStopTrap;
-                }
-                if (!priv) {
-                    L.trap(GEVO_TRAP_INTERNAL);
-                    return kStopTrap;
-                }
-                A.priv[A.priv_off[p] + static_cast<size_t>(eff) * A.n_inst + L.il] = vp;
-            }
-            break;
-        }
-        case GEVO_OP_GETINDEX: {
-            uint32_t pt, off, idx;
-            if (!L.pointer(in.a, pt, off))
-                return kStopTrap;
-            if ((pt == GEVO_TAG_PTR_SHARED ? 1u : 0u) != in.want) {
-                L.trap(GEVO_TRAP_GETINDEX_SPACE);
-                return kStopTrap;
-            }
-            if (!L.scalar(in.b, GEVO_TAG_I32, idx))
-                return kStopTrap;
-            ok = L.set(in.res, pt, off + idx);
-            break;
-        }
-        case GEVO_OP_TID:
-            ok = L.set(in.res, GEVO_TAG_I32, static_cast<uint32_t>(L.tid));
-            break;
-        case GEVO_OP_NTHREADS:
-            ok = L.set(in.res, GEVO_TAG_I32, static_cast<uint32_t>(A.threads));
-            break;
-        case GEVO_OP_CONST:
-            ok = L.set(in.res, L.G(in.a), L.P(in.a));
-            break;
-        default:
-            L.trap(GEVO_TRAP_UNEXPECTED_OP);
+        if (!ok) {
+            refund(L, th, b, ip + 1, s_cost);
             return kStopTrap;
         }
-        if (!ok)
-            return kStopTrap;
         ++th.ip;
     }
 }
 
-} // namespace
-
-
-// Error metric of one completed instance (compute_error, src/vm.cpp:536-556):
-// 1.0 on any structural mismatch (resolved on the host per test), else the max
-// over oracle elements of the clamped relative difference. max() is exact and
-// order-free, so the per-buffer early return of the reference is not needed.
-__device__ double instance_error(const InterpArgs& A, const Lane& L) {
-    if (A.static_err[L.t])
-        return 1.0;
-    const uint32_t nt = static_cast<uint32_t>(A.n_tests);
-    double worst = 0.0;
-    for (int32_t e = A.entry_begin[L.t]; e < A.entry_begin[L.t + 1]; ++e) {
-        const OracleEntryDev en = A.entries[e];
-        const uint32_t p = static_cast<uint32_t>(en.param);
-        const bool priv = (L.writable >> p) & 1ull;
-        for (int32_t k = 0; k < en.size; ++k) {
-            const uint32_t cw =
-                priv ? A.priv[A.priv_off[p] + static_cast<size_t>(k) * A.n_inst + L.il]
-                     : __ldg(A.pool + A.pool_off[p] + static_cast<size_t>(k) * nt + L.t);
-            const uint32_t ow = __ldg(A.pool + en.off + static_cast<size_t>(k) * nt + L.t);
-            const double d = rel_diff(word_to_double(cw, en.elem), word_to_double(ow, en.elem));
-            worst = (worst < d) ? d : worst;
-        }
-        if (worst >= 1.0)
-            return 1.0;
-    }
-    return worst;
+__device__ __forceinline__ uint32_t status_of(uint32_t code) {
+    return code == GEVO_BUDGET_EXCEEDED ? GEVO_STATUS_BUDGET
+           : code == GEVO_SKIPPED      ? GEVO_STATUS_SKIPPED
+                                       : GEVO_STATUS_TRAP;
 }
 
-__device__ __forceinline__ void reset_values(Lane& L) {
+template <bool kSmem>
+__device__ __forceinline__ void reset_values(Lane<kSmem>& L) {
     for (uint32_t s = 0; s < L.n_values; ++s)
-        L.G(s) = GEVO_TAG_UNDEF;
+        L.W(s, 0, GEVO_TAG_UNDEF);
 }
 
 // Machine::run for one instance (src/vm.cpp:114-150). Returns the status.
-__device__ uint32_t run_instance(const InterpArgs& A, Lane& L, const gevo_variant& var,
+template <bool kSmem>
+__device__ uint32_t run_instance(const InterpArgs& A, Lane<kSmem>& L, const gevo_variant& var,
                                  const int64_t* s_cost, const volatile int32_t* first_fail) {
     const int32_t T = A.threads;
     if (!(var.flags & GEVO_VAR_HAS_SYNC)) {
@@ -483,12 +957,10 @@ __device__ uint32_t run_instance(const InterpArgs& A, Lane& L, const gevo_varian
         for (int32_t tid = 0; tid < T; ++tid) {
             reset_values(L);
             L.tid = tid;
-            Thread th{0, 0, -1, 0, 0};
+            Thread th{0, 0, -1, 0, 0, false};
             const int r = run_thread(A, L, th, s_cost, first_fail);
             if (r == kStopTrap)
-                return L.code_out == GEVO_BUDGET_EXCEEDED ? GEVO_STATUS_BUDGET
-                       : L.code_out == GEVO_SKIPPED      ? GEVO_STATUS_SKIPPED
-                                                         : GEVO_STATUS_TRAP;
+                return status_of(L.code_out);
             if (r != kStopRet) {
                 L.trap(GEVO_TRAP_INTERNAL);
                 return GEVO_STATUS_TRAP;
@@ -520,22 +992,20 @@ __device__ uint32_t run_instance(const InterpArgs& A, Lane& L, const gevo_varian
                 th.prev = A.ts_prev[at];
                 th.executed = A.ts_exec[at];
                 th.bar = 0;
+                th.slow = false;
                 const size_t vbase = static_cast<size_t>(tid) * A.ts_slots;
                 if (st == kTsFresh) {
                     reset_values(L);
                 } else {
                     for (uint32_t s = 0; s < L.n_values; ++s) {
                         const size_t sv = (vbase + s) * n + L.il;
-                        L.G(s) = A.ts_tag[sv];
-                        L.P(s) = A.ts_val[sv];
+                        L.W(s, A.ts_val[sv], A.ts_tag[sv]);
                     }
                 }
                 L.tid = tid;
                 const int r = run_thread(A, L, th, s_cost, first_fail);
                 if (r == kStopTrap)
-                    return L.code_out == GEVO_BUDGET_EXCEEDED ? GEVO_STATUS_BUDGET
-                           : L.code_out == GEVO_SKIPPED      ? GEVO_STATUS_SKIPPED
-                                                             : GEVO_STATUS_TRAP;
+                    return status_of(L.code_out);
                 A.ts_pos[at] = (th.block << 16) | th.ip;
                 A.ts_prev[at] = th.prev;
                 A.ts_exec[at] = th.executed;
@@ -544,8 +1014,9 @@ __device__ uint32_t run_instance(const InterpArgs& A, Lane& L, const gevo_varian
                 if (r == kStopSync) {
                     for (uint32_t s = 0; s < L.n_values; ++s) {
                         const size_t sv = (vbase + s) * n + L.il;
-                        A.ts_tag[sv] = L.G(s);
-                        A.ts_val[sv] = L.P(s);
+                        const uint2 v = L.V(s);
+                        A.ts_tag[sv] = static_cast<uint8_t>(v.y);
+                        A.ts_val[sv] = v.x;
                     }
                 }
             }
@@ -570,30 +1041,72 @@ __device__ uint32_t run_instance(const InterpArgs& A, Lane& L, const gevo_varian
     }
 }
 
-template <int kLanes>
-__global__ void __launch_bounds__(kLanes) interp_kernel(const __grid_constant__ InterpArgs A) {
-    extern __shared__ __align__(16) unsigned char smem[];
+// Error metric of one completed instance (compute_error, src/vm.cpp:536-556):
+// 1.0 on any structural mismatch (resolved on the host per test), else the max
+// over oracle elements of the clamped relative difference. max() is exact and
+// order-free, so the per-buffer early return of the reference is not needed.
+template <bool kSmem>
+__device__ double instance_error(const InterpArgs& A, const Lane<kSmem>& L) {
+    if (A.static_err[L.t])
+        return 1.0;
+    const uint32_t nt = static_cast<uint32_t>(A.n_tests);
+    double worst = 0.0;
+    for (int32_t e = A.entry_begin[L.t]; e < A.entry_begin[L.t + 1]; ++e) {
+        const OracleEntryDev en = A.entries[e];
+        const uint32_t p = static_cast<uint32_t>(en.param);
+        const bool priv = (L.writable >> p) & 1ull;
+        for (int32_t k = 0; k < en.size; ++k) {
+            const uint32_t cw =
+                priv ? A.priv[A.priv_off[p] + static_cast<size_t>(k) * A.n_inst + L.il]
+                     : __ldg(A.pool + A.pool_off[p] + static_cast<size_t>(k) * nt + L.t);
+            const uint32_t ow = __ldg(A.pool + en.off + static_cast<size_t>(k) * nt + L.t);
+            const double d = rel_diff(word_to_double(cw, en.elem), word_to_double(ow, en.elem));
+            worst = (worst < d) ? d : worst;
+        }
+        if (worst >= 1.0)
+            return 1.0;
+    }
+    return worst;
+}
+
+} // namespace
+
+template <bool kSmem>
+__global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ InterpArgs A) {
     __shared__ int64_t s_cost[GEVO_COST_CLASSES];
     if (threadIdx.x < GEVO_COST_CLASSES)
         s_cost[threadIdx.x] = A.cost[threadIdx.x];
     __syncthreads();
 
-    const uint32_t il = blockIdx.x * kLanes + threadIdx.x;
-    if (il >= A.n_inst)
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp;
+    const uint32_t vl = gw / A.warps_per_variant; // variant, local to the launch
+    const uint32_t t = (gw % A.warps_per_variant) * 32 + lane;
+    if (vl >= A.n_var || t >= static_cast<uint32_t>(A.n_tests))
         return;
-    const uint64_t gi = A.inst_begin + il;
+    const uint32_t v = A.v_begin + vl;
     const uint32_t nt = static_cast<uint32_t>(A.n_tests);
+    const uint32_t il = vl * nt + t;
+    const uint64_t gi = static_cast<uint64_t>(v) * nt + t;
 
-    Lane L;
-    L.v = static_cast<uint32_t>(gi / nt);
-    L.t = static_cast<uint32_t>(gi % nt);
+    Lane<kSmem> L;
+    L.v = v;
+    L.t = t;
     L.il = il;
-    L.stride = kLanes;
-    L.pay = reinterpret_cast<uint32_t*>(smem) + threadIdx.x;
-    L.tag = smem + static_cast<size_t>(4) * kLanes * A.max_slots + threadIdx.x;
+    if (kSmem) {
+        L.gvf = nullptr;
+        L.base = warp * A.row_lanes * A.max_slots + (lane & (A.row_lanes - 1));
+        L.row = A.row_lanes;
+    } else {
+        L.gvf = A.vf;
+        L.base = il;
+        L.row = A.n_inst;
+    }
     L.cost = 0;
     L.ir = 0;
     L.poll = 2048;
+    L.jumps = 0;
+    L.spin_dbg = 0;
     L.code_out = GEVO_OK;
     L.aux = 0;
     L.writable = 0;
@@ -602,38 +1115,36 @@ __global__ void __launch_bounds__(kLanes) interp_kernel(const __grid_constant__ 
     const volatile int32_t* first_fail = A.first_fail;
     uint32_t status;
     double error = -1.0;
-    const uint8_t setup = A.setup_code[L.t];
-    if (A.early_exit && first_fail[L.v] < static_cast<int32_t>(L.t)) {
+    const uint8_t setup = A.setup_code[t];
+    if (A.early_exit && first_fail[v] < static_cast<int32_t>(t)) {
         L.code_out = GEVO_SKIPPED;
         status = GEVO_STATUS_SKIPPED;
     } else if (setup != GEVO_OK) {
         // Machine ctor failure: trap with cost 0 (src/vm.cpp:516-520).
         L.code_out = setup;
-        L.aux = A.setup_aux[L.t];
+        L.aux = A.setup_aux[t];
         status = GEVO_STATUS_TRAP;
     } else {
-        const gevo_variant var = A.variants[L.v];
+        const gevo_variant var = A.variants[v];
         const uint32_t P = static_cast<uint32_t>(A.n_params);
         L.code = A.insts + var.inst_base;
-        L.blk = A.blocks + var.block_base;
+        L.dblk = A.dblocks + var.block_base;
         L.arm = A.arms + var.arm_base;
         L.n_values = var.n_values;
+        L.n_slots = var.n_slots;
         L.writable = var.writable;
         const uint32_t lit_begin = var.n_values + P + 2;
         L.stage_base = lit_begin + var.n_lits;
 
         // Parameters (bound per test), poison slots, literal pool.
-        const size_t tp0 = static_cast<size_t>(L.t) * P;
-        for (uint32_t p = 0; p < P; ++p) {
-            L.G(var.n_values + p) = A.param_tag[tp0 + p];
-            L.P(var.n_values + p) = A.param_payload[tp0 + p];
-        }
-        L.G(var.n_values + P) = GEVO_TAG_POISON_PARAM;
-        L.G(var.n_values + P + 1) = GEVO_TAG_POISON_MISSING;
-        for (uint32_t k = 0; k < var.n_lits; ++k) {
-            L.G(lit_begin + k) = __ldg(A.lit_tag + var.lit_base + k);
-            L.P(lit_begin + k) = __ldg(A.lit_payload + var.lit_base + k);
-        }
+        const size_t tp0 = static_cast<size_t>(t) * P;
+        for (uint32_t p = 0; p < P; ++p)
+            L.W(var.n_values + p, A.param_payload[tp0 + p], A.param_tag[tp0 + p]);
+        L.W(var.n_values + P, 0, GEVO_TAG_POISON_PARAM);
+        L.W(var.n_values + P + 1, 0, GEVO_TAG_POISON_MISSING);
+        for (uint32_t k = 0; k < var.n_lits; ++k)
+            L.W(lit_begin + k, __ldg(A.lit_payload + var.lit_base + k),
+                __ldg(A.lit_tag + var.lit_base + k));
         // Private copies of the buffers this variant may store to
         // (Machine ctor copies every global buffer, src/vm.cpp:96-97; read-only
         // ones are served from the shared test pool).
@@ -642,7 +1153,7 @@ __global__ void __launch_bounds__(kLanes) interp_kernel(const __grid_constant__ 
             const int32_t rows = A.buf_size[tp0 + p];
             for (int32_t e = 0; e < rows; ++e)
                 A.priv[A.priv_off[p] + static_cast<size_t>(e) * A.n_inst + il] =
-                    __ldg(A.pool + A.pool_off[p] + static_cast<size_t>(e) * nt + L.t);
+                    __ldg(A.pool + A.pool_off[p] + static_cast<size_t>(e) * nt + t);
         }
         for (int32_t w = 0; w < A.shared_words; ++w)
             A.sh_tag[static_cast<size_t>(w) * A.n_inst + il] = GEVO_TAG_UNDEF;
@@ -659,12 +1170,39 @@ __global__ void __launch_bounds__(kLanes) interp_kernel(const __grid_constant__ 
     rec.aux = L.aux;
     rec.status = static_cast<uint8_t>(status);
     rec.code = static_cast<uint8_t>(L.code_out);
-    rec.pad[0] = rec.pad[1] = 0;
+    rec.pad[0] = static_cast<uint8_t>(L.jumps);
+    rec.pad[1] = static_cast<uint8_t>(L.spin_dbg);
     A.rec[gi] = rec;
 
     if (A.early_exit && status != GEVO_STATUS_SKIPPED &&
         (status != GEVO_STATUS_COMPLETED || error > A.tolerance))
-        atomicMin(A.first_fail + L.v, static_cast<int32_t>(L.t));
+        atomicMin(A.first_fail + v, static_cast<int32_t>(t));
+}
+
+// Per-launch block records: {start, len | nphi << 16, cost of the block under
+// the launch's cost table} (one thread per variant).
+struct CostTableArg {
+    int64_t c[GEVO_COST_CLASSES];
+};
+
+__global__ void block_cost_kernel(const gevo_variant* __restrict__ variants,
+                                  const gevo_block* __restrict__ blocks,
+                                  const gevo_inst* __restrict__ insts, uint32_t n_variants,
+                                  const CostTableArg ct, uint4* __restrict__ out) {
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n_variants)
+        return;
+    const gevo_variant var = variants[v];
+    for (uint32_t b = 0; b < var.n_blocks; ++b) {
+        const gevo_block g = blocks[var.block_base + b];
+        int64_t c = 0;
+        for (uint32_t j = 0; j < g.len; ++j)
+            c += ct.c[insts[var.inst_base + g.start + j].cls];
+        const uint64_t u = static_cast<uint64_t>(c);
+        out[var.block_base + b] =
+            make_uint4(g.start, static_cast<uint32_t>(g.len) | (static_cast<uint32_t>(g.nphi) << 16),
+                       static_cast<uint32_t>(u), static_cast<uint32_t>(u >> 32));
+    }
 }
 
 // evaluate_fitness reduction (src/vm.cpp:558-579), one thread per variant,
@@ -737,25 +1275,55 @@ cudaError_t launch_error(const uint32_t* cand, const uint32_t* orc, const uint8_
     return cudaGetLastError();
 }
 
-// Lanes per CTA: 128 while the value file fits (5 B per slot per lane),
-// 32 for very large variants.
-int interp_lanes(uint32_t max_slots) { return max_slots <= kMaxSlots128 ? 128 : 32; }
+LaunchShape interp_shape(int32_t n_tests, uint32_t max_slots) {
+    LaunchShape s;
+    uint32_t row = 1;
+    while (row < 32 && row < static_cast<uint32_t>(n_tests))
+        row <<= 1;
+    s.row_lanes = row;
+    const size_t per_warp = static_cast<size_t>(row) * 8 * max_slots;
+    s.vf_global = per_warp > kSmemBudget;
+    if (s.vf_global) {
+        s.warps_per_cta = 4;
+        s.smem = 0;
+        return s;
+    }
+    uint32_t w = 4;
+    while (w > 1 && per_warp * w > kSmemBudget)
+        w >>= 1;
+    s.warps_per_cta = w;
+    s.smem = per_warp * w;
+    return s;
+}
+
+cudaError_t launch_block_cost(const gevo_block* blocks, const gevo_inst* insts,
+                              const gevo_variant* variants, uint32_t n_variants,
+                              const int64_t* cost_table, uint4* out, cudaStream_t stream) {
+    if (n_variants == 0)
+        return cudaSuccess;
+    CostTableArg ct;
+    for (int i = 0; i < GEVO_COST_CLASSES; ++i)
+        ct.c[i] = cost_table[i];
+    block_cost_kernel<<<(n_variants + 127) / 128, 128, 0, stream>>>(variants, blocks, insts,
+                                                                    n_variants, ct, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_interp(const InterpArgs& A, cudaStream_t stream) {
-    const int lanes = interp_lanes(A.max_slots);
-    const size_t smem = static_cast<size_t>(5) * lanes * A.max_slots;
-    const unsigned grid = (A.n_inst + lanes - 1) / lanes;
-    if (grid == 0)
+    if (A.n_var == 0)
         return cudaSuccess;
-    if (lanes == 128) {
-        cudaFuncSetAttribute(interp_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        interp_kernel<128><<<grid, 128, smem, stream>>>(A);
-    } else {
-        cudaFuncSetAttribute(interp_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        interp_kernel<32><<<grid, 32, smem, stream>>>(A);
+    const LaunchShape s = interp_shape(A.n_tests, A.max_slots);
+    const uint64_t warps = static_cast<uint64_t>(A.n_var) * A.warps_per_variant;
+    const unsigned grid = static_cast<unsigned>((warps + s.warps_per_cta - 1) / s.warps_per_cta);
+    if (s.vf_global) {
+        interp_kernel<false><<<grid, 32 * s.warps_per_cta, 0, stream>>>(A);
+        return cudaGetLastError();
     }
+    const cudaError_t e = cudaFuncSetAttribute(
+        interp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s.smem));
+    if (e != cudaSuccess)
+        return e;
+    interp_kernel<true><<<grid, 32 * s.warps_per_cta, s.smem, stream>>>(A);
     return cudaGetLastError();
 }
 

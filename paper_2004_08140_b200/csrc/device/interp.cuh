@@ -25,6 +25,7 @@ struct InterpArgs {
     const gevo_arm* arms;
     const uint32_t* lit_payload;
     const uint8_t* lit_tag;
+    const uint4* dblocks;          // [batch block] {start, len | nphi << 16, cost (int64)}
     uint32_t n_variants;
 
     // suite
@@ -49,10 +50,16 @@ struct InterpArgs {
     int64_t cost[GEVO_COST_CLASSES];
     double tolerance;
 
-    // instances handled by this launch: [inst_begin, inst_begin + n_inst)
-    uint64_t inst_begin;
-    uint32_t n_inst;
-    uint32_t max_slots; // value-file capacity per lane (dynamic smem sizing)
+    // variants handled by this launch: [v_begin, v_begin + n_var); instance
+    // il = (v - v_begin) * n_tests + test indexes the per-launch scratch.
+    uint32_t v_begin;
+    uint32_t n_var;
+    uint32_t n_inst;                // n_var * n_tests
+    uint32_t max_slots;             // value-file capacity per lane
+    uint32_t warps_per_variant;     // ceil(n_tests / 32)
+    uint32_t row_lanes;             // lanes per value-file row (pow2, <= 32)
+    uint32_t vf_global;             // value file in global scratch (too large for smem)
+    uint2* vf;                      // global value file [inst][slot] when vf_global
 
     // per-instance scratch (instance-interleaved: index = row * n_inst + local)
     uint32_t* priv;                 // private copies of writable global buffers
@@ -68,17 +75,46 @@ struct InterpArgs {
     uint8_t* ts_tag;
     uint32_t ts_slots;              // max dynamic slots (batch max n_values)
 
+    // spin accelerator scratch ([slot][inst]); null disables it
+    uint32_t* sp_base;              // payload at the reference iterate
+    uint8_t* sp_btag;
+    uint32_t* sp_delta;             // per-iteration stride hypothesis
+    uint32_t* sp_cur;               // stride of the running abstract iterate
+    uint8_t* sp_hvary;              // hypothesis: slot may vary (path-irrelevant)
+    uint8_t* sp_cvary;              // abstract iterate: slot value is varying
+    uint32_t* sp_log;               // [kSpinLog][inst] x 3: store-log key, old payload, old tag|flags
+    uint32_t* sp_ld;                // [kSpinLog][inst] load-log keys
+    int64_t spin_threshold;         // per-thread executed count that arms it
+
     // outputs
     gevo_test_record* rec;          // [variant * n_tests + test]
     int32_t* first_fail;            // [variant] (early-exit mode)
     int32_t early_exit;
+    uint64_t* counters;             // [2]: accelerated spins, jumped instructions (nullable)
 };
 
-// Value-file capacity limits (dynamic shared memory, 227 KB per CTA).
-constexpr uint32_t kMaxSlots128 = 350;
-constexpr uint32_t kMaxSlots32 = 1400;
+// Memory words one abstract iterate may store to / load from.
+constexpr uint32_t kSpinLog = 8;
 
-int interp_lanes(uint32_t max_slots);
+// Value slots a variant may use (value file in shared memory or global scratch).
+constexpr uint32_t kMaxSlots = GEVO_MAX_SLOTS;
+
+// Shared memory available to the value file of one CTA.
+constexpr size_t kSmemBudget = 200 * 1024;
+
+struct LaunchShape {
+    uint32_t row_lanes;
+    uint32_t warps_per_cta;
+    size_t smem;
+    bool vf_global;
+};
+LaunchShape interp_shape(int32_t n_tests, uint32_t max_slots);
+
+// Builds the per-launch block records (block table + cost under the launch's
+// cost table) that the interpreter reads with one 16-byte load per block entry.
+cudaError_t launch_block_cost(const gevo_block* blocks, const gevo_inst* insts,
+                              const gevo_variant* variants, uint32_t n_variants,
+                              const int64_t* cost_table, uint4* out, cudaStream_t stream);
 cudaError_t launch_interp(const InterpArgs& A, cudaStream_t stream);
 cudaError_t launch_error(const uint32_t* cand, const uint32_t* orc, const uint8_t* elem, uint32_t n,
                          double* out, cudaStream_t stream);

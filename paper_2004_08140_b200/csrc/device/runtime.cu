@@ -72,6 +72,8 @@ struct DeviceImpl {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     DevBuf blob, rec, vrec, first_fail, priv, sh_tag, sh_val;
     DevBuf ts_pos, ts_prev, ts_exec, ts_stop, ts_val, ts_tag;
+    DevBuf bcost, vf, sp_base, sp_btag, sp_delta, sp_cur, sp_hvary, sp_cvary, sp_log, sp_ld,
+        counters;
     DevBuf rank;
     PinnedBuf h_blob, h_vrec, h_rec;
     size_t scratch_budget = size_t(8) << 30; // bytes of per-instance scratch per launch
@@ -164,7 +166,7 @@ namespace {
 
 // Scratch bytes one instance needs in a launch.
 size_t scratch_per_instance(const SuiteImage& S, uint64_t writable_any, const ExecImage& ex,
-                            bool any_sync, uint32_t max_values) {
+                            bool any_sync, uint32_t max_values, uint32_t max_slots, bool vf_global) {
     size_t b = 0;
     for (int p = 0; p < S.n_params; ++p)
         if ((writable_any >> p) & 1ull)
@@ -172,13 +174,11 @@ size_t scratch_per_instance(const SuiteImage& S, uint64_t writable_any, const Ex
     b += 5 * static_cast<size_t>(std::max(ex.shared_words, 0));
     if (any_sync)
         b += static_cast<size_t>(ex.threads) * (4 + 4 + 8 + 4 + 5 * static_cast<size_t>(max_values));
+    b += 15 * static_cast<size_t>(max_slots) + 16 * gevo::kSpinLog; // spin accelerator
+    if (vf_global)
+        b += 8 * static_cast<size_t>(max_slots);
     return b;
 }
-
-struct Launch {
-    gevo::InterpArgs A;
-    size_t chunk;
-};
 
 // Fills everything but the batch pointers and the per-chunk window.
 gevo::InterpArgs base_args(DeviceSuite& suite, const ExecImage& ex, const EvalOptions& opt) {
@@ -222,14 +222,25 @@ void bind_batch(gevo::InterpArgs& A, const void* dblob, const gevo_batch_header&
     A.ts_slots = std::max<uint32_t>(h.max_values, 1);
 }
 
-// Launches the interpreter over all instances in scratch-bounded chunks, then
+// Spin accelerator arms after this many instructions of one simulated thread
+// (clean corpus threads run <= ~1000; GEVO_SPIN_THRESHOLD=0 disables it).
+int64_t spin_threshold() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("GEVO_SPIN_THRESHOLD");
+        return e ? std::atoll(e) : int64_t(8192);
+    }();
+    return v;
+}
+
+// Launches the interpreter over all variants in scratch-bounded chunks, then
 // the per-variant reduction. Records land in dev.rec / dev.vrec.
 int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const gevo_batch_header& h,
                uint64_t writable_any, const ExecImage& ex, const EvalOptions& opt,
                cudaStream_t s) {
     const SuiteImage& S = suite.image();
-    if (h.max_slots > gevo::kMaxSlots32)
+    if (h.max_slots > gevo::kMaxSlots)
         throw std::invalid_argument("variant value file exceeds the device limit");
+    const uint32_t T = static_cast<uint32_t>(std::max(S.n_tests, 1));
     const uint64_t total = static_cast<uint64_t>(h.n_variants) * static_cast<uint64_t>(S.n_tests);
     dev.rec.reserve(std::max<size_t>(total * sizeof(gevo_test_record), 16));
     dev.vrec.reserve(std::max<size_t>(h.n_variants * sizeof(gevo_variant_record), 16));
@@ -239,28 +250,42 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
               "memset first_fail");
     A.rec = dev.rec.as<gevo_test_record>();
     A.first_fail = dev.first_fail.as<int32_t>();
+    int launches = 0;
+
+    // Block costs under this launch's cost table.
+    dev.bcost.reserve(std::max<size_t>(h.n_blocks * sizeof(uint4), 16));
+    check(gevo::launch_block_cost(A.blocks, A.insts, A.variants, h.n_variants, ex.cost.data(),
+                                  dev.bcost.as<uint4>(), s),
+          "block_cost_kernel launch");
+    ++launches;
+    A.dblocks = dev.bcost.as<uint4>();
+
+    const gevo::LaunchShape shape = gevo::interp_shape(S.n_tests, A.max_slots);
+    A.row_lanes = shape.row_lanes;
+    A.vf_global = shape.vf_global ? 1 : 0;
+    A.warps_per_variant = (T + 31) / 32;
 
     const size_t per = std::max<size_t>(
-        scratch_per_instance(S, writable_any, ex, h.any_sync != 0, h.max_values), 1);
-    size_t chunk = std::min<uint64_t>(total, std::max<size_t>(dev.scratch_budget / per, 128));
-    chunk = std::min<size_t>(chunk, size_t(1) << 30);
-    int launches = 0;
-    // scratch layout for a chunk
+        scratch_per_instance(S, writable_any, ex, h.any_sync != 0, h.max_values, A.max_slots,
+                             shape.vf_global),
+        1);
+    // chunk = variants per launch
+    size_t chunk = std::max<size_t>(dev.scratch_budget / (per * T), 64);
+    chunk = std::min<size_t>(chunk, std::max<uint32_t>(h.n_variants, 1));
+    const size_t cap = chunk * T; // instances per launch window
     size_t priv_words = 0;
-    for (int p = 0; p < S.n_params; ++p) {
-        A.priv_off[p] = priv_words * chunk;
+    for (int p = 0; p < S.n_params; ++p)
         if ((writable_any >> p) & 1ull)
             priv_words += static_cast<size_t>(S.pool_rows[static_cast<size_t>(p)]);
-    }
-    dev.priv.reserve(std::max<size_t>(priv_words * chunk * 4, 16));
+    dev.priv.reserve(std::max<size_t>(priv_words * cap * 4, 16));
     const size_t sw = static_cast<size_t>(std::max(ex.shared_words, 0));
-    dev.sh_tag.reserve(std::max<size_t>(sw * chunk, 16));
-    dev.sh_val.reserve(std::max<size_t>(sw * chunk * 4, 16));
+    dev.sh_tag.reserve(std::max<size_t>(sw * cap, 16));
+    dev.sh_val.reserve(std::max<size_t>(sw * cap * 4, 16));
     A.priv = dev.priv.as<uint32_t>();
     A.sh_tag = dev.sh_tag.as<uint8_t>();
     A.sh_val = dev.sh_val.as<uint32_t>();
     if (h.any_sync) {
-        const size_t tn = static_cast<size_t>(ex.threads) * chunk;
+        const size_t tn = static_cast<size_t>(ex.threads) * cap;
         dev.ts_pos.reserve(tn * 4);
         dev.ts_prev.reserve(tn * 4);
         dev.ts_exec.reserve(tn * 8);
@@ -274,21 +299,46 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
         A.ts_val = dev.ts_val.as<uint32_t>();
         A.ts_tag = dev.ts_tag.as<uint8_t>();
     }
-    for (uint64_t begin = 0; begin < total; begin += chunk) {
-        A.inst_begin = begin;
-        A.n_inst = static_cast<uint32_t>(std::min<uint64_t>(chunk, total - begin));
-        // priv_off is laid out for `chunk` rows; the last chunk may be shorter,
-        // so keep the stride equal to the chunk capacity.
+    if (shape.vf_global) {
+        dev.vf.reserve(cap * A.max_slots * 8);
+        A.vf = dev.vf.as<uint2>();
+    }
+    const int64_t thr = spin_threshold();
+    if (thr > 0) {
+        const size_t n = cap * A.max_slots;
+        dev.sp_base.reserve(n * 4);
+        dev.sp_btag.reserve(n);
+        dev.sp_delta.reserve(n * 4);
+        dev.sp_cur.reserve(n * 4);
+        dev.sp_hvary.reserve(n);
+        dev.sp_cvary.reserve(n);
+        dev.sp_log.reserve(cap * gevo::kSpinLog * 3 * 4);
+        dev.sp_ld.reserve(cap * gevo::kSpinLog * 4);
+        A.sp_hvary = dev.sp_hvary.as<uint8_t>();
+        A.sp_cvary = dev.sp_cvary.as<uint8_t>();
+        A.sp_log = dev.sp_log.as<uint32_t>();
+        A.sp_ld = dev.sp_ld.as<uint32_t>();
+        A.sp_base = dev.sp_base.as<uint32_t>();
+        A.sp_btag = dev.sp_btag.as<uint8_t>();
+        A.sp_delta = dev.sp_delta.as<uint32_t>();
+        A.sp_cur = dev.sp_cur.as<uint32_t>();
+        A.spin_threshold = thr;
+    }
+    if (!dev.counters.ptr) {
+        dev.counters.reserve(16);
+        check(cudaMemsetAsync(dev.counters.ptr, 0, 16, s), "counters");
+    }
+    A.counters = dev.counters.as<uint64_t>();
+    for (uint64_t vb = 0; vb < h.n_variants; vb += chunk) {
         gevo::InterpArgs L = A;
-        L.n_inst = A.n_inst;
-        if (L.n_inst != chunk) {
-            // Re-lay out the private regions for the shorter window.
-            size_t words = 0;
-            for (int p = 0; p < S.n_params; ++p) {
-                L.priv_off[p] = words * L.n_inst;
-                if ((writable_any >> p) & 1ull)
-                    words += static_cast<size_t>(S.pool_rows[static_cast<size_t>(p)]);
-            }
+        L.v_begin = static_cast<uint32_t>(vb);
+        L.n_var = static_cast<uint32_t>(std::min<uint64_t>(chunk, h.n_variants - vb));
+        L.n_inst = L.n_var * T;
+        size_t words = 0;
+        for (int p = 0; p < S.n_params; ++p) {
+            L.priv_off[p] = words * L.n_inst;
+            if ((writable_any >> p) & 1ull)
+                words += static_cast<size_t>(S.pool_rows[static_cast<size_t>(p)]);
         }
         check(gevo::launch_interp(L, s), "interp_kernel launch");
         ++launches;
@@ -326,7 +376,7 @@ EvalResult evaluate(DeviceSuite& suite, BatchImage& batch, const ExecImage& exec
 
     dev.h_blob.reserve(blob.size());
     std::memcpy(dev.h_blob.ptr, blob.data(), blob.size());
-    dev.blob.reserve(blob.size());
+    dev.blob.reserve(blob.size() + 64); // slack: the interpreter prefetches one record ahead
     check(cudaEventRecord(dev.ev0, s), "event");
     check(cudaMemcpyAsync(dev.blob.ptr, dev.h_blob.ptr, blob.size(), cudaMemcpyHostToDevice, s),
           "blob H2D");
@@ -357,7 +407,7 @@ EvalResult evaluate(DeviceSuite& suite, BatchImage& batch, const ExecImage& exec
     size_t chunk = total;
     if (opt.want_outputs && total) {
         // Only supported when every instance ran in one launch window.
-        if (R.launches != 2)
+        if (R.launches != 3)
             throw std::invalid_argument("want_outputs needs a single-launch batch");
         size_t words = 0;
         for (int p = 0; p < S.n_params; ++p)
@@ -436,13 +486,13 @@ std::shared_ptr<ResidentBatch> make_resident(DeviceSuite& suite, BatchImage& bat
     const auto& blob = batch.blob();
     rb->h = batch.header();
     rb->writable = writable_union(batch);
-    rb->blob.reserve(blob.size());
+    rb->blob.reserve(blob.size() + 64);
     check(cudaMemcpy(rb->blob.ptr, blob.data(), blob.size(), cudaMemcpyHostToDevice), "resident");
     return rb;
 }
 
 float evaluate_resident(ResidentBatch& rb, const ExecImage& exec, const EvalOptions& opt,
-                        float* interp_ms, std::vector<gevo_variant_record>* out) {
+                        float* interp_ms, std::vector<gevo_variant_record>* out, int* launches) {
     Device& devh = rb.suite->device();
     std::lock_guard<std::mutex> g(devh.lock());
     DeviceImpl& dev = devh.impl();
@@ -451,7 +501,9 @@ float evaluate_resident(ResidentBatch& rb, const ExecImage& exec, const EvalOpti
     gevo::InterpArgs A = base_args(*rb.suite, exec, opt);
     bind_batch(A, rb.blob.ptr, rb.h);
     check(cudaEventRecord(dev.ev0, s), "event");
-    launch_all(dev, *rb.suite, A, rb.h, rb.writable, exec, opt, s);
+    const int nl = launch_all(dev, *rb.suite, A, rb.h, rb.writable, exec, opt, s);
+    if (launches)
+        *launches = nl;
     check(cudaEventRecord(dev.ev2, s), "event");
     if (out) {
         out->resize(rb.h.n_variants);
@@ -465,6 +517,19 @@ float evaluate_resident(ResidentBatch& rb, const ExecImage& exec, const EvalOpti
     if (interp_ms)
         *interp_ms = ms;
     return ms;
+}
+
+void spin_counters(Device& devh, uint64_t out[2], bool reset) {
+    std::lock_guard<std::mutex> g(devh.lock());
+    DeviceImpl& dev = devh.impl();
+    out[0] = out[1] = 0;
+    if (!dev.counters.ptr)
+        return;
+    check(cudaSetDevice(dev.ordinal), "cudaSetDevice");
+    check(cudaMemcpyAsync(out, dev.counters.ptr, 16, cudaMemcpyDeviceToHost, dev.stream), "counters");
+    if (reset)
+        check(cudaMemsetAsync(dev.counters.ptr, 0, 16, dev.stream), "counters");
+    check(cudaStreamSynchronize(dev.stream), "counters");
 }
 
 ParetoRank rank_on_device(Device& devh, const std::vector<FitnessVector>& fits, bool single_group) {

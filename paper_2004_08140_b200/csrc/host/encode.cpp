@@ -347,18 +347,19 @@ void BatchImage::add(const Kernel& k) {
             g.t0 = g.t1 = -1;
             switch (in.op) {
             case Opcode::ICmp: case Opcode::FCmp:
-                g.want = static_cast<uint8_t>(in.pred);
+                g.aux = static_cast<uint8_t>(in.pred);
+                g.otag = in.op == Opcode::ICmp ? GEVO_TAG_I32 : GEVO_TAG_F32;
                 g.a = ref(in, 0);
                 g.b = ref(in, 1);
                 break;
             case Opcode::Select:
-                g.want = scalar_tag(in.type.kind);
+                g.aux = scalar_tag(in.type.kind);
                 g.a = ref(in, 0);
                 g.b = ref(in, 1);
                 g.c = ref(in, 2);
                 break;
             case Opcode::Load:
-                g.want = scalar_tag(in.type.kind);
+                g.aux = scalar_tag(in.type.kind);
                 g.a = ref(in, 0);
                 g.b = ref(in, 1);
                 break;
@@ -368,22 +369,35 @@ void BatchImage::add(const Kernel& k) {
                 g.c = ref(in, 2);
                 break;
             case Opcode::GetIndex:
-                g.want = (in.type.kind == TypeKind::Ptr && in.type.space == MemSpace::Shared) ? 1 : 0;
+                g.aux = (in.type.kind == TypeKind::Ptr && in.type.space == MemSpace::Shared) ? 1 : 0;
                 g.a = ref(in, 0);
                 g.b = ref(in, 1);
                 break;
             case Opcode::Phi: {
-                g.a = static_cast<uint16_t>(arms_.size() - var.arm_base);
-                const size_t n = std::min(in.operands.size(), in.labels.size());
                 // Arms beyond the label list can never match a predecessor.
-                g.b = static_cast<uint16_t>(n);
-                for (size_t a = 0; a < n; ++a)
-                    arms_.push_back(gevo_arm{static_cast<int16_t>(k.block_index(in.labels[a])),
-                                             ref(in, a)});
+                const size_t n = std::min(in.operands.size(), in.labels.size());
+                if (n > 255)
+                    throw std::invalid_argument("phi with more than 255 arms");
+                g.aux = static_cast<uint8_t>(n);
+                if (n <= 2) {
+                    if (n > 0) {
+                        g.a = ref(in, 0);
+                        g.t0 = static_cast<int16_t>(k.block_index(in.labels[0]));
+                    }
+                    if (n > 1) {
+                        g.b = ref(in, 1);
+                        g.t1 = static_cast<int16_t>(k.block_index(in.labels[1]));
+                    }
+                } else {
+                    g.c = static_cast<uint16_t>(arms_.size() - var.arm_base);
+                    for (size_t a = 0; a < n; ++a)
+                        arms_.push_back(gevo_arm{static_cast<int16_t>(k.block_index(in.labels[a])),
+                                                 ref(in, a)});
+                }
                 break;
             }
             case Opcode::Br:
-                g.want = in.labels.size() == 2 ? 2 : 1;
+                g.aux = in.labels.size() == 2 ? 2 : 1;
                 if (!in.labels.empty())
                     g.t0 = static_cast<int16_t>(k.block_index(in.labels[0]));
                 if (in.labels.size() == 2) {
@@ -402,7 +416,13 @@ void BatchImage::add(const Kernel& k) {
                 break;
             case Opcode::Ret: case Opcode::Tid: case Opcode::NThreads:
                 break;
-            default: // two-operand arithmetic
+            case Opcode::Add: case Opcode::Sub: case Opcode::Mul: case Opcode::SDiv:
+                g.otag = GEVO_TAG_I32;
+                g.a = ref(in, 0);
+                g.b = ref(in, 1);
+                break;
+            default: // float arithmetic
+                g.otag = GEVO_TAG_F32;
                 g.a = ref(in, 0);
                 g.b = ref(in, 1);
                 break;

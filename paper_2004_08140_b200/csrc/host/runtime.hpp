@@ -81,7 +81,11 @@ std::shared_ptr<ResidentBatch> make_resident(DeviceSuite& suite, BatchImage& bat
 // (CUDA events on the launch stream) and fills `interp_ms` with the share of
 // the interpreter kernel alone.
 float evaluate_resident(ResidentBatch& rb, const ExecImage& exec, const EvalOptions& opt,
-                        float* interp_ms, std::vector<gevo_variant_record>* out);
+                        float* interp_ms, std::vector<gevo_variant_record>* out,
+                        int* launches = nullptr);
+
+// Spin-accelerator counters of a device: {loops jumped, instructions skipped}.
+void spin_counters(Device& dev, uint64_t out[2], bool reset);
 
 // GPU NSGA ranking (front + crowding + fronts in reference order).
 ParetoRank rank_on_device(Device& dev, const std::vector<FitnessVector>& fits, bool single_group);

@@ -1,9 +1,13 @@
+# GPU round trip: parity tests, bench, launch list (+ optional full ncu capture).
 mkdir -p gpurun_out
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -30 > gpurun_out/pytest_gpu.txt
 cat gpurun_out/pytest_gpu.txt
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
+timeout 600 python bench.py ${BENCH_ARGS:-} > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
+if [ -n "$NCU_LIST" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench_ncu.log 2>&1; tail -2 gpurun_out/bench_ncu.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:interp_kernel -s 3 -c 1 -o gpurun_out/prof_interp python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; tail -5 gpurun_out/ncu_full.log
-ls -la gpurun_out
+fi
+if [ -n "$NCU_FULL" ]; then
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:interp_kernel -s ${NCU_SKIP:-3} -c 1 -o gpurun_out/prof_interp python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; tail -3 gpurun_out/ncu_full.log
+fi
+ls gpurun_out
