@@ -224,6 +224,7 @@ struct Spin {
     int64_t p, c;      // per-iteration instructions / cost
     int64_t H;         // iterations the abstract proof must cover
     uint32_t nst, nld; // store / load log entries of the abstract iterate
+    uint32_t retries;  // abstract iterates re-run with a widened hypothesis
 };
 
 template <bool kSmem>
@@ -543,6 +544,7 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kSmem>& 
         S.c0 = L.cost;
         S.nst = 0;
         S.nld = 0;
+        S.retries = 0;
         S.H = (A.budget - th.executed) / p;
         if (S.H < 3) {
             spin_abandon(S, th, L, 4);
@@ -556,17 +558,49 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kSmem>& 
         spin_abandon(S, th, L, 5);
         return;
     }
+    // Slots whose observed behaviour contradicts the hypothesis (a changing
+    // "fixed" slot, a broken stride) become varying and the abstract iterate
+    // is re-run from S2; varying only grows, so this converges.
+    bool retry = false;
     for (uint32_t x = 0; x < L.n_values; ++x) {
         const uint2 v = L.V(x);
         const size_t at = sp_at(A, L, x);
-        bool ok = A.sp_btag[at] == v.y;
-        if (ok && !A.sp_hvary[at])
-            ok = !A.sp_cvary[at] && v.x - A.sp_base[at] == A.sp_delta[at] &&
-                 A.sp_cur[at] == A.sp_delta[at];
-        if (!ok) {
+        if (A.sp_btag[at] != v.y) {
             spin_abandon(S, th, L, 6);
             return;
         }
+        if (!A.sp_hvary[at] && (A.sp_cvary[at] || v.x - A.sp_base[at] != A.sp_delta[at] ||
+                                A.sp_cur[at] != A.sp_delta[at])) {
+            A.sp_hvary[at] = 1;
+            retry = true;
+        }
+    }
+    if (retry) {
+        if (++S.retries > 4) {
+            spin_abandon(S, th, L, 9);
+            return;
+        }
+        for (uint32_t x = 0; x < L.n_values; ++x) {
+            const size_t at = sp_at(A, L, x);
+            const uint32_t vary = A.sp_hvary[at];
+            const uint32_t d = vary ? 0u : A.sp_delta[at];
+            A.sp_delta[at] = d;
+            A.sp_base[at] = L.V(x).x;
+            A.sp_cur[at] = d;
+            A.sp_cvary[at] = static_cast<uint8_t>(vary);
+        }
+        for (uint32_t x = L.n_values; x < L.n_slots; ++x) {
+            A.sp_cur[sp_at(A, L, x)] = 0;
+            A.sp_cvary[sp_at(A, L, x)] = 0;
+        }
+        S.e0 = th.executed;
+        S.c0 = L.cost;
+        S.nst = 0;
+        S.nld = 0;
+        S.H = (A.budget - th.executed) / S.p;
+        if (S.H < 3)
+            spin_abandon(S, th, L, 4);
+        return;
     }
     // memory: fixed-value words are back to their S1 contents; no fixed load
     // reads a word that holds varying data
