@@ -205,6 +205,7 @@ def b200_arm(args):
     import numpy as np
     import torch
     import paper_2004_08140_b200 as gevo
+    from paper_2004_08140_b200 import dist as gdist
 
     rank, local, world = dist_env()
     torch.cuda.set_device(local)
@@ -248,18 +249,10 @@ def b200_arm(args):
         # NCCL all-gather of per-variant fitness (cost_mean, error_max, accepted)
         # then the GPU non-dominated sort of the gathered population.
         nonlocal gathered_front
-        rec = np.concatenate(vrec_list)
-        fit = np.stack([rec["cost_mean"], rec["error_max"],
-                        rec["accepted"].astype(np.float64)], axis=1)
-        t = torch.from_numpy(np.ascontiguousarray(fit)).to("cuda", non_blocking=False)
-        if world > 1:
-            import torch.distributed as dist
-            out = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device="cuda")
-            dist.all_gather_into_tensor(out, t)
-            t = out.reshape(-1, 3)
-        g = t.cpu().numpy()
-        keep = g[:, 2] > 0.5
-        front, _, _ = gevo.rank(g[keep, 0], g[keep, 1])
+        rows = gdist.fitness_rows(np.concatenate(vrec_list))
+        g = gdist.allgather_fitness(rows, device="cuda") if world > 1 else rows
+        cost, err, _ = gdist.accepted_fitness(g)
+        front, _, _ = gevo.rank(cost, err)
         gathered_front = front
 
     timed_launches = [0]

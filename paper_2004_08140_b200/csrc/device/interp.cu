@@ -52,6 +52,8 @@ extern __shared__ __align__(16) uint2 g_vfs[]; // value files of the CTA's warps
 namespace {
 
 constexpr int kStopRet = 1, kStopSync = 2, kStopTrap = 3;
+// Fewest iterations a spin-accelerator jump may cover.
+constexpr int64_t kSpinMinJump = 4;
 // ts_stop encodings (multi-phase kernels)
 constexpr uint32_t kTsFresh = 0, kTsResume = 3u << 16; // never run / resume after barrier
 constexpr uint32_t kTsRet = 1u << 16, kTsSync = 2u << 16;
@@ -223,6 +225,7 @@ struct Spin {
     int64_t e0, c0;    // executed / lane cost at the reference iterate
     int64_t p, c;      // per-iteration instructions / cost
     int64_t H;         // iterations the abstract proof must cover
+    int64_t K;         // iterations every compare of the iterate provably keeps its outcome
     uint32_t nst, nld; // store / load log entries of the abstract iterate
     uint32_t retries;  // abstract iterates re-run with a widened hypothesis
 };
@@ -304,25 +307,47 @@ __device__ __forceinline__ bool slot_strided(uint32_t tag) {
     return tag == GEVO_TAG_I32 || is_ptr_tag(tag);
 }
 
-// Does (X + k*sx) pred (Y + k*sy) keep its k = 0 outcome for all k in [0, H]
-// with neither side leaving the int32 range?
-__device__ bool cmp_constant(int32_t X, int32_t sx, int32_t Y, int32_t sy, uint32_t pred,
-                             int64_t H) {
-    const int64_t xH = static_cast<int64_t>(X) + H * sx;
-    const int64_t yH = static_cast<int64_t>(Y) + H * sy;
-    if (xH < INT32_MIN || xH > INT32_MAX || yH < INT32_MIN || yH > INT32_MAX)
-        return false;
+// Largest K in [0, H] such that (X + k*sx) pred (Y + k*sy) keeps its k = 0
+// outcome for every k in [0, K] with neither side leaving the int32 range.
+__device__ int64_t cmp_horizon(int32_t X, int32_t sx, int32_t Y, int32_t sy, uint32_t pred,
+                               int64_t H) {
+    // int32 range: |side(k)| stays representable for k <= K
+    auto range = [](int64_t v, int64_t s, int64_t h) -> int64_t {
+        if (s > 0)
+            return min(h, (static_cast<int64_t>(INT32_MAX) - v) / s);
+        if (s < 0)
+            return min(h, (v - static_cast<int64_t>(INT32_MIN)) / -s);
+        return h;
+    };
+    H = range(X, sx, range(Y, sy, H));
     const int64_t f0 = static_cast<int64_t>(X) - Y;
     const int64_t slope = static_cast<int64_t>(sx) - sy;
-    if (slope == 0)
-        return true;
-    if (pred <= 1) { // eq / ne: no root of f in [0, H]
+    if (slope == 0 || H <= 0)
+        return H;
+    if (pred <= 1) { // eq / ne: the outcome changes at the first root of f in [1, H]
+        if (f0 == 0)
+            return 0;
         if (f0 % slope != 0)
-            return true;
+            return H;
         const int64_t r = -f0 / slope;
-        return r < 0 || r > H;
+        return (r < 1 || r > H) ? H : r - 1;
     }
-    return cmp(static_cast<int64_t>(X), static_cast<int64_t>(Y), pred) == cmp(xH, yH, pred);
+    // lt / le / gt / ge of an affine f: monotone in k, at most one change
+    const bool c0 = cmp(static_cast<int64_t>(X), static_cast<int64_t>(Y), pred);
+    auto same = [&](int64_t k) {
+        return cmp(static_cast<int64_t>(X) + k * sx, static_cast<int64_t>(Y) + k * sy, pred) == c0;
+    };
+    if (same(H))
+        return H;
+    int64_t lo = 0, hi = H; // same(lo), !same(hi)
+    while (hi - lo > 1) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (same(mid))
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
 }
 
 template <bool kSmem>
@@ -408,9 +433,12 @@ __device__ __forceinline__ bool spin_track(const InterpArgs& A, const Lane<kSmem
             const uint2 x = L.V(a), y = L.V(b);
             if (x.y != GEVO_TAG_I32 || y.y != GEVO_TAG_I32)
                 return false;
-            if (!cmp_constant(static_cast<int32_t>(x.x), static_cast<int32_t>(sa),
-                              static_cast<int32_t>(y.x), static_cast<int32_t>(sb), f_aux(r), S.H))
+            const int64_t K = cmp_horizon(static_cast<int32_t>(x.x), static_cast<int32_t>(sa),
+                                          static_cast<int32_t>(y.x), static_cast<int32_t>(sb),
+                                          f_aux(r), S.K);
+            if (K < kSpinMinJump)
                 return false;
+            S.K = K;
         }
         break;
     case GEVO_OP_SELECT: {
@@ -546,6 +574,7 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kSmem>& 
         S.nld = 0;
         S.retries = 0;
         S.H = (A.budget - th.executed) / p;
+        S.K = S.H;
         if (S.H < 3) {
             spin_abandon(S, th, L, 4);
             return;
@@ -598,6 +627,7 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kSmem>& 
         S.nst = 0;
         S.nld = 0;
         S.H = (A.budget - th.executed) / S.p;
+        S.K = S.H;
         if (S.H < 3)
             spin_abandon(S, th, L, 4);
         return;
@@ -621,7 +651,23 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kSmem>& 
             return;
         }
     }
-    const int64_t n = (A.budget - th.executed) / S.p;
+    // Jump n whole iterations. Up to the budget, the record depends on the path
+    // only; a partial jump (a compare flips before the budget runs out) resumes
+    // an execution that may complete, so every value it leaves behind must be
+    // exact: no varying slot, no varying store.
+    const int64_t n_budget = (A.budget - th.executed) / S.p;
+    const int64_t n = min(n_budget, S.K);
+    if (n < n_budget) {
+        bool vary = n < kSpinMinJump;
+        for (uint32_t x = 0; x < L.n_values && !vary; ++x)
+            vary = A.sp_hvary[sp_at(A, L, x)] != 0;
+        for (uint32_t j = 0; j < S.nst && !vary; ++j)
+            vary = (A.sp_log[log_at(A, L, j, 2)] & 0x100) != 0;
+        if (vary) {
+            spin_abandon(S, th, L, 10);
+            return;
+        }
+    }
     if (n > 0) {
         for (uint32_t x = 0; x < L.n_values; ++x) {
             const size_t at = sp_at(A, L, x);
@@ -642,7 +688,14 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kSmem>& 
         }
     }
     S.mode = 0;
-    S.next = INT64_MAX;
+    if (n < n_budget) {
+        // interpret past the flip, then look for the next affine stretch
+        S.attempts = 0;
+        S.skip = 0;
+        S.next = th.executed + 2 * S.p + 16;
+    } else {
+        S.next = INT64_MAX;
+    }
 }
 
 // Phi arm for predecessor `prev` (first matching arm, vm.cpp:311-323);

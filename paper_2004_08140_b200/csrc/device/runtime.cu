@@ -223,11 +223,11 @@ void bind_batch(gevo::InterpArgs& A, const void* dblob, const gevo_batch_header&
 }
 
 // Spin accelerator arms after this many instructions of one simulated thread
-// (clean corpus threads run <= ~1000; GEVO_SPIN_THRESHOLD=0 disables it).
+// (clean corpus threads run <= ~750; GEVO_SPIN_THRESHOLD=0 disables it).
 int64_t spin_threshold() {
     static const int64_t v = [] {
         const char* e = std::getenv("GEVO_SPIN_THRESHOLD");
-        return e ? std::atoll(e) : int64_t(8192);
+        return e ? std::atoll(e) : int64_t(1024);
     }();
     return v;
 }

@@ -32,11 +32,20 @@ def _oracle_tests(gevo, bench, n, seed):
     return tests, cfg
 
 
-@pytest.mark.parametrize("bench,count", [("hot-branch", 160), ("bfs-load", 160),
-                                         ("hot-memo", 96), ("lud-store", 96)])
-def test_spinner_records_match_oracle(gevo, bench, count):
+@pytest.mark.parametrize("bench,count,pick", [
+    ("hot-branch", 160, None), ("bfs-load", 160, None), ("hot-memo", 96, None),
+    ("lud-store", 96, None),
+    # bench.py's own hot-branch sample: 748 is a 1000-trip loop per thread that
+    # ends in a trap (partial jumps), 410 a budget spinner
+    ("hot-branch", 1024, [748, 410, 874, 303] + list(range(0, 1024, 9))),
+    ("nw-sync", 1024, [774, 415, 689, 852, 505] + list(range(1, 1024, 13)))])
+def test_spinner_records_match_oracle(gevo, bench, count, pick):
     seed = gevo.train_seed(1)
-    cands = gevo.sample_candidates(bench, count, 11, 4)
+    if pick is None:
+        cands = gevo.sample_candidates(bench, count, 11, 4)
+    else:
+        every = gevo.sample_candidates(bench, count, 1, 4)
+        cands = [every[i] for i in pick]
     suite = gevo.Suite.from_benchmark(bench, 2, seed)
     cfg = suite.exec_config()
     batch = suite.batch()
@@ -62,5 +71,5 @@ def test_spinner_records_match_oracle(gevo, bench, count):
             else:
                 assert hex_double(float(got["error"])) == hex_double(exp["error"]), where
             budget_runs += exp["status"] == "budget"
-    if bench in ("hot-branch", "bfs-load"):
+    if bench in ("hot-branch", "bfs-load") and pick is None:
         assert budget_runs > 0 and jumped > 0
