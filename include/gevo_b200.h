@@ -44,6 +44,8 @@ typedef struct {
 /* Evaluation flags. */
 #define GEVO_EVAL_EARLY_EXIT 1u /* stop a variant's remaining tests after its first failure */
 #define GEVO_EVAL_TESTS 2u      /* fill per-test records */
+#define GEVO_EVAL_SEQUENTIAL 4u /* force the sequential-lane interpreter (one lane runs all
+                                   simulated threads of an instance in id order) */
 
 typedef struct {
     float device_ms;       /* CUDA-event time of the interpreter + reduction launches */
@@ -67,6 +69,10 @@ int gevo_set_stream(void* stream);
  * last reset: out2[0] = budget-bound loops jumped, out2[1] = instructions
  * skipped by those jumps (counted in the records as executed). */
 int gevo_spin_counters(uint64_t* out2, int reset);
+/* Thread-parallel interpreter counters since the last reset: out2[0] =
+ * instances re-executed in thread-id order after a same-phase cross-thread
+ * read/write conflict, out2[1] = instances run by the thread-parallel kernel. */
+int gevo_tp_counters(uint64_t* out2, int reset);
 void gevo_free(void* p);
 
 /* ---- test suites (uploaded once, resident in HBM) ------------------------

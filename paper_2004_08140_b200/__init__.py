@@ -31,7 +31,7 @@ assert TEST_RECORD.itemsize == 32 and VARIANT_RECORD.itemsize == 48
 
 STATUS_COMPLETED, STATUS_TRAP, STATUS_BUDGET, STATUS_SKIPPED = 0, 1, 2, 3
 FAIL_TOLERANCE = 0xFF
-EVAL_EARLY_EXIT, EVAL_TESTS = 1, 2
+EVAL_EARLY_EXIT, EVAL_TESTS, EVAL_SEQUENTIAL = 1, 2, 4
 COST_FIELDS = ("arith", "cmp", "select_op", "phi", "constant", "br", "intrinsic", "getindex",
                "load_shared", "store_shared", "load_global", "store_global", "sync", "ret")
 DEFAULT_COSTS = (1, 1, 1, 1, 1, 1, 1, 1, 4, 4, 20, 20, 8, 1)
@@ -95,6 +95,7 @@ _SIGNATURES = [
     ("gevo_last_error", ctypes.c_char_p, []),
     ("gevo_set_stream", ctypes.c_int, [_vp]),
     ("gevo_spin_counters", ctypes.c_int, [_vp, ctypes.c_int]),
+    ("gevo_tp_counters", ctypes.c_int, [_vp, ctypes.c_int]),
     ("gevo_free", None, [_vp]),
     ("gevo_suite_from_benchmark", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _u64, ctypes.c_int,
                                                  ctypes.POINTER(_vp)]),
@@ -246,6 +247,14 @@ def set_stream(stream_ptr: int) -> None:
     _check(lib().gevo_set_stream(ctypes.c_void_p(stream_ptr or None)))
 
 
+def tp_counters(reset: bool = False) -> tuple:
+    """(instances re-run in thread-id order, instances run) by the
+    thread-parallel interpreter."""
+    out = (ctypes.c_uint64 * 2)()
+    _check(lib().gevo_tp_counters(ctypes.cast(out, ctypes.c_void_p), 1 if reset else 0))
+    return out[0], out[1]
+
+
 def spin_counters(reset: bool = False) -> tuple:
     """(loops jumped, instructions skipped) by the spin accelerator."""
     out = (ctypes.c_uint64 * 2)()
@@ -332,12 +341,14 @@ class Batch:
         return ctypes.string_at(p.value, n.value)
 
     def eval(self, cfg: ExecConfig, tolerance: float = 0.0, early_exit: bool = False,
-             tests: bool = False):
-        """Returns (variant_records, test_records | None, EvalStats)."""
+             tests: bool = False, sequential: bool = False):
+        """Returns (variant_records, test_records | None, EvalStats).
+        sequential=True forces the sequential-lane interpreter."""
         n, t = len(self), self.suite.n_tests
         vrec = np.zeros(n, VARIANT_RECORD)
         trec = np.zeros(n * t, TEST_RECORD) if tests else None
-        flags = (EVAL_EARLY_EXIT if early_exit else 0) | (EVAL_TESTS if tests else 0)
+        flags = ((EVAL_EARLY_EXIT if early_exit else 0) | (EVAL_TESTS if tests else 0) |
+                 (EVAL_SEQUENTIAL if sequential else 0))
         st = EvalStats()
         _check(lib().gevo_eval(self._h, ctypes.byref(cfg), tolerance, flags,
                                vrec.ctypes.data_as(ctypes.c_void_p),

@@ -144,6 +144,10 @@ int gevo_spin_counters(uint64_t* out2, int reset) {
     return guard([&] { b200::spin_counters(b200::Device::default_device(), out2, reset != 0); });
 }
 
+int gevo_tp_counters(uint64_t* out2, int reset) {
+    return guard([&] { b200::tp_counters(b200::Device::default_device(), out2, reset != 0); });
+}
+
 const char* gevo_last_error(void) { return g_error.c_str(); }
 
 void gevo_free(void* p) { std::free(p); }
@@ -238,6 +242,7 @@ int gevo_eval(gevo_batch* b, const gevo_exec_config* cfg, double tolerance, uint
         b200::EvalOptions opt;
         opt.tolerance = tolerance;
         opt.early_exit = (flags & GEVO_EVAL_EARLY_EXIT) != 0;
+        opt.sequential = (flags & GEVO_EVAL_SEQUENTIAL) != 0;
         opt.want_tests = out_tests && (flags & GEVO_EVAL_TESTS);
         const b200::EvalResult r =
             b200::evaluate(*b->suite->suite, *b->image, b200::exec_image(exec_from(cfg)), opt);
@@ -261,6 +266,7 @@ int gevo_eval_resident(gevo_batch* b, const gevo_exec_config* cfg, double tolera
         b200::EvalOptions opt;
         opt.tolerance = tolerance;
         opt.early_exit = (flags & GEVO_EVAL_EARLY_EXIT) != 0;
+        opt.sequential = (flags & GEVO_EVAL_SEQUENTIAL) != 0;
         std::vector<gevo_variant_record> recs;
         float interp = 0.0f;
         int launches = 0;

@@ -51,7 +51,7 @@ extern __shared__ __align__(16) uint2 g_vfs[]; // value files of the CTA's warps
 
 namespace {
 
-constexpr int kStopRet = 1, kStopSync = 2, kStopTrap = 3;
+constexpr int kStopRet = 1, kStopSync = 2, kStopTrap = 3, kStopAbort = 4, kStopIdle = 0;
 // Fewest iterations a spin-accelerator jump may cover.
 constexpr int64_t kSpinMinJump = 4;
 // ts_stop encodings (multi-phase kernels)
@@ -111,10 +111,15 @@ __device__ __forceinline__ bool bad_tag(uint32_t t) {
 }
 
 // Value file of one lane: slot s lives at index base + s * row of the CTA's
-// shared array (kSmem) or of the global scratch array.
-template <bool kSmem>
+// shared array (kM >= 1) or of the global scratch array (kM == 0).
+// kM: 0 = sequential lanes, value file in global scratch; 1 = sequential
+// lanes, value file in shared memory; 2 = thread-parallel lanes (one lane per
+// simulated thread, instance memory in shared-memory cells, see interp_tp_kernel).
+template <int kM>
 struct Lane {
-    uint2* gvf;      // global value file (when !kSmem)
+    static constexpr bool kSmem = kM >= 1;
+    static constexpr bool kTP = kM == 2;
+    uint2* gvf;      // global value file (kM == 0)
     uint32_t base;   // element index of slot 0
     uint32_t row;
     // program
@@ -127,11 +132,22 @@ struct Lane {
     uint64_t writable;
     // instance
     uint32_t v, t, il;
+    uint32_t sl;     // spin-accelerator scratch column (instance, or lane when kTP)
     int32_t tid;
+    // thread-parallel lanes (kTP)
+    uint2* cells;            // instance memory cells [word][cta instance] in shared memory
+    uint32_t cell_row;       // cta instances per word row
+    uint32_t* rbits;         // read / write bitsets of this lane: chunk k at [k * bit_row]
+    uint32_t* wbits;
+    uint32_t bit_row;
+    uint32_t epoch;          // phase number (max-tid-wins store rule)
+    bool seq;                // sequential fallback: plain stores, no conflict tracking
+    const volatile int32_t* min_stop; // lowest tid of the instance that stopped this phase
     // counters
     int64_t cost;
     int64_t ir;
     int32_t poll;
+    uint32_t poll2;
     uint32_t jumps;   // spin-accelerator jumps (diagnostic, saturating)
     uint32_t spin_dbg;// last spin-accelerator abandon reason (diagnostic)
     // trap
@@ -149,6 +165,8 @@ struct Lane {
         else
             gvf[base + s * row] = make_uint2(payload, tag);
     }
+    // kTP: memory cell of word w of the instance
+    __device__ __forceinline__ uint2* cell(uint32_t w) const { return cells + w * cell_row; }
 
     __device__ __forceinline__ bool trap(uint32_t c, int32_t x = 0) {
         code_out = c;
@@ -230,8 +248,8 @@ struct Spin {
     uint32_t retries;  // abstract iterates re-run with a widened hypothesis
 };
 
-template <bool kSmem>
-__device__ __forceinline__ int64_t suffix_cost(const Lane<kSmem>& L, const Blk& b, uint32_t from,
+template <int kM>
+__device__ __forceinline__ int64_t suffix_cost(const Lane<kM>& L, const Blk& b, uint32_t from,
                                                const int64_t* s_cost) {
     int64_t c = 0;
     for (uint32_t j = from; j < b.len; ++j)
@@ -240,8 +258,8 @@ __device__ __forceinline__ int64_t suffix_cost(const Lane<kSmem>& L, const Blk& 
 }
 
 // Charges instructions [from, len) of the current block on entry / resume.
-template <bool kSmem>
-__device__ __forceinline__ void charge_block(const InterpArgs& A, Lane<kSmem>& L, Thread& th,
+template <int kM>
+__device__ __forceinline__ void charge_block(const InterpArgs& A, Lane<kM>& L, Thread& th,
                                              const Blk& b, int64_t bcost, uint32_t from,
                                              const int64_t* s_cost) {
     const int64_t n = static_cast<int64_t>(b.len) - from;
@@ -256,8 +274,8 @@ __device__ __forceinline__ void charge_block(const InterpArgs& A, Lane<kSmem>& L
 }
 
 // Refunds instructions [from, len) charged on entry that will not run.
-template <bool kSmem>
-__device__ __forceinline__ void refund(Lane<kSmem>& L, Thread& th, const Blk& b, uint32_t from,
+template <int kM>
+__device__ __forceinline__ void refund(Lane<kM>& L, Thread& th, const Blk& b, uint32_t from,
                                        const int64_t* s_cost) {
     if (th.slow || from >= b.len)
         return;
@@ -268,8 +286,8 @@ __device__ __forceinline__ void refund(Lane<kSmem>& L, Thread& th, const Blk& b,
 }
 
 // Per-instruction charge (exact mode): cost and budget before any effect.
-template <bool kSmem>
-__device__ __forceinline__ bool charge_one(const InterpArgs& A, Lane<kSmem>& L, Thread& th,
+template <int kM>
+__device__ __forceinline__ bool charge_one(const InterpArgs& A, Lane<kM>& L, Thread& th,
                                            uint32_t cls, const int64_t* s_cost) {
     L.cost += s_cost[cls];
     ++L.ir;
@@ -288,13 +306,13 @@ __device__ __forceinline__ bool charge_one(const InterpArgs& A, Lane<kSmem>& L, 
 // conditions, compare operands, addresses, divisors, tags) must be affine
 // with a provably constant outcome.
 
-template <bool kSmem>
-__device__ __forceinline__ size_t sp_at(const InterpArgs& A, const Lane<kSmem>& L, uint32_t s) {
-    return static_cast<size_t>(s) * A.n_inst + L.il;
+template <int kM>
+__device__ __forceinline__ size_t sp_at(const InterpArgs& A, const Lane<kM>& L, uint32_t s) {
+    return static_cast<size_t>(s) * A.n_spin + L.sl;
 }
 
-template <bool kSmem>
-__device__ __forceinline__ void spin_abandon(Spin& S, const Thread& th, Lane<kSmem>& L,
+template <int kM>
+__device__ __forceinline__ void spin_abandon(Spin& S, const Thread& th, Lane<kM>& L,
                                              uint32_t why) {
     S.mode = 0;
     ++S.attempts;
@@ -350,18 +368,18 @@ __device__ int64_t cmp_horizon(int32_t X, int32_t sx, int32_t Y, int32_t sy, uin
     return lo;
 }
 
-template <bool kSmem>
-__device__ __forceinline__ uint32_t spin_stride(const InterpArgs& A, const Lane<kSmem>& L,
+template <int kM>
+__device__ __forceinline__ uint32_t spin_stride(const InterpArgs& A, const Lane<kM>& L,
                                                 uint32_t s) {
     return s < L.n_slots ? A.sp_cur[sp_at(A, L, s)] : 0u;
 }
-template <bool kSmem>
-__device__ __forceinline__ uint32_t spin_vary(const InterpArgs& A, const Lane<kSmem>& L,
+template <int kM>
+__device__ __forceinline__ uint32_t spin_vary(const InterpArgs& A, const Lane<kM>& L,
                                               uint32_t s) {
     return s < L.n_slots ? A.sp_cvary[sp_at(A, L, s)] : 0u;
 }
-template <bool kSmem>
-__device__ __forceinline__ void spin_set(const InterpArgs& A, const Lane<kSmem>& L, uint32_t s,
+template <int kM>
+__device__ __forceinline__ void spin_set(const InterpArgs& A, const Lane<kM>& L, uint32_t s,
                                          uint32_t stride, uint32_t vary) {
     if (s < L.n_slots) {
         A.sp_cur[sp_at(A, L, s)] = stride;
@@ -377,16 +395,20 @@ __device__ __forceinline__ uint32_t mem_key(uint32_t ptag, int64_t eff) {
     return (space << 24) | static_cast<uint32_t>(eff);
 }
 
-template <bool kSmem>
-__device__ __forceinline__ size_t log_at(const InterpArgs& A, const Lane<kSmem>& L, uint32_t i,
+template <int kM>
+__device__ __forceinline__ size_t log_at(const InterpArgs& A, const Lane<kM>& L, uint32_t i,
                                          uint32_t field) {
-    return (static_cast<size_t>(field) * kSpinLog + i) * A.n_inst + L.il;
+    return (static_cast<size_t>(field) * kSpinLog + i) * A.n_spin + L.sl;
 }
 
 // Current memory word (payload, tag) behind a key.
-template <bool kSmem>
-__device__ __forceinline__ uint2 mem_word(const InterpArgs& A, const Lane<kSmem>& L, uint32_t key) {
+template <int kM>
+__device__ __forceinline__ uint2 mem_word(const InterpArgs& A, const Lane<kM>& L, uint32_t key) {
     const uint32_t eff = key & 0xFFFFFF, space = key >> 24;
+    if (Lane<kM>::kTP) {
+        const uint2 c = *L.cell(space == 0x80 ? eff : A.cell_off[space - 1] + eff);
+        return make_uint2(c.x, c.y & 0xFF);
+    }
     if (space == 0x80) {
         const size_t at = static_cast<size_t>(eff) * A.n_inst + L.il;
         return make_uint2(A.sh_val[at], A.sh_tag[at]);
@@ -398,8 +420,8 @@ __device__ __forceinline__ uint2 mem_word(const InterpArgs& A, const Lane<kSmem>
 // Stride transfer of one instruction of the abstract iterate, called before
 // its concrete execution (operands still hold their k = 0 values). Returns
 // false when the instruction breaks the proof.
-template <bool kSmem>
-__device__ __forceinline__ bool spin_track(const InterpArgs& A, const Lane<kSmem>& L,
+template <int kM>
+__device__ __forceinline__ bool spin_track(const InterpArgs& A, const Lane<kM>& L,
                                            const uint4 r, Spin& S) {
     const uint32_t op = f_op(r), a = f_a(r), b = f_b(r), c = f_c(r), res = f_res(r);
     uint32_t out = 0, vout = 0;
@@ -513,8 +535,8 @@ __device__ __forceinline__ bool spin_track(const InterpArgs& A, const Lane<kSmem
 }
 
 // Protocol step at every completed block entry (phis done).
-template <bool kSmem>
-__device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kSmem>& L, Thread& th,
+template <int kM>
+__device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, Thread& th,
                                               Spin& S) {
     if (S.mode == 0) {
         if (th.executed < S.next)
@@ -700,8 +722,8 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kSmem>& 
 
 // Phi arm for predecessor `prev` (first matching arm, vm.cpp:311-323);
 // returns false when no arm matches.
-template <bool kSmem>
-__device__ __forceinline__ bool phi_arm(const Lane<kSmem>& L, const uint4 r, int32_t prev,
+template <int kM>
+__device__ __forceinline__ bool phi_arm(const Lane<kM>& L, const uint4 r, int32_t prev,
                                         uint32_t& ref) {
     const uint32_t n = f_aux(r);
     if (n <= 2) {
@@ -727,8 +749,8 @@ __device__ __forceinline__ bool phi_arm(const Lane<kSmem>& L, const uint4 r, int
 }
 
 // enter_block (vm.cpp:293-333): charge and stage every leading phi, then write.
-template <bool kSmem>
-__device__ bool enter_block(const InterpArgs& A, Lane<kSmem>& L, Thread& th, const int64_t* s_cost,
+template <int kM>
+__device__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Thread& th, const int64_t* s_cost,
                             int32_t target, Blk& b, Spin& S) {
     th.prev = th.block;
     th.block = target;
@@ -798,8 +820,8 @@ __device__ bool enter_block(const InterpArgs& A, Lane<kSmem>& L, Thread& th, con
 }
 
 // Memory instructions (vm.cpp:238-283, 447-460): off the hot dispatch path.
-template <bool kSmem>
-__device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kSmem>& L, const uint4 r) {
+template <int kM>
+__device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const uint4 r) {
     const uint32_t op = f_op(r);
     uint2 p;
     if (!L.pointer(f_a(r), p))
@@ -818,6 +840,74 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kSmem>& L, cons
     }
     const int64_t eff = static_cast<int64_t>(static_cast<int32_t>(p.x)) +
                         static_cast<int64_t>(static_cast<int32_t>(ix.x));
+    if (Lane<kM>::kTP) {
+        // Instance memory cells (shared words, then writable global buffers).
+        uint32_t w;
+        if (p.y == GEVO_TAG_PTR_SHARED) {
+            if (eff < 0 || eff >= A.shared_words)
+                return L.trap(GEVO_TRAP_SHARED_OOB);
+            w = static_cast<uint32_t>(eff);
+        } else {
+            const uint32_t prm = p.y & 0x3F;
+            const size_t tp = static_cast<size_t>(L.t) * A.n_params + prm;
+            if (eff < 0 || eff >= __ldg(A.buf_size + tp))
+                return L.trap(GEVO_TRAP_GLOBAL_OOB);
+            const uint32_t elem = __ldg(A.buf_elem + tp);
+            if (op == GEVO_OP_LOAD) {
+                if (elem != f_aux(r))
+                    return L.trap(GEVO_TRAP_GLOBAL_LOAD_TYPE);
+                if (!((L.writable >> prm) & 1ull))
+                    return L.set(f_res(r), __ldg(A.pool + A.pool_off[prm] +
+                                                 static_cast<size_t>(eff) * A.n_tests + L.t),
+                                 elem);
+            } else {
+                if (elem != val.y)
+                    return L.trap(GEVO_TRAP_GLOBAL_STORE_TYPE);
+                if (!((L.writable >> prm) & 1ull))
+                    return L.trap(GEVO_TRAP_INTERNAL);
+            }
+            w = A.cell_off[prm] + static_cast<uint32_t>(eff);
+        }
+        uint2* c = L.cell(w);
+        const uint32_t bit = 1u << (w & 31);
+        if (op == GEVO_OP_LOAD) {
+            if (!L.seq)
+                L.rbits[(w >> 5) * L.bit_row] |= bit;
+            const uint2 x = *c;
+            if (p.y == GEVO_TAG_PTR_SHARED) {
+                const uint32_t wt = x.y & 0xFF;
+                if (wt == GEVO_TAG_UNDEF)
+                    return L.trap(GEVO_TRAP_SHARED_UNINIT);
+                if (wt != f_aux(r))
+                    return L.trap(GEVO_TRAP_SHARED_TYPE);
+            }
+            return L.set(f_res(r), x.x, x.y & 0xFF);
+        }
+        if (L.seq) {
+            *c = make_uint2(val.x, val.y);
+            return true;
+        }
+        L.wbits[(w >> 5) * L.bit_row] |= bit;
+        // Same-phase stores of several simulated threads: the highest thread id
+        // wins, and a thread's own stores land in program order (the
+        // reference runs threads one after another, src/vm.cpp:121-142).
+        const uint32_t me = static_cast<uint32_t>(L.tid) + 1;
+        const uint32_t meta = val.y | (me << 8) | (L.epoch << 16);
+        unsigned long long* cp = reinterpret_cast<unsigned long long*>(c);
+        const unsigned long long want =
+            (static_cast<unsigned long long>(meta) << 32) | val.x;
+        unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(cp);
+        for (;;) {
+            const uint32_t m = static_cast<uint32_t>(cur >> 32);
+            if ((m >> 16) == L.epoch && ((m >> 8) & 0xFF) > me)
+                break;
+            const unsigned long long prev = atomicCAS(cp, cur, want);
+            if (prev == cur)
+                break;
+            cur = prev;
+        }
+        return true;
+    }
     if (p.y == GEVO_TAG_PTR_SHARED) {
         if (eff < 0 || eff >= A.shared_words)
             return L.trap(GEVO_TRAP_SHARED_OOB);
@@ -858,8 +948,8 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kSmem>& L, cons
 }
 
 // Non-arithmetic straight-line instructions (select, getindex, intrinsics, const).
-template <bool kSmem>
-__device__ __forceinline__ bool misc_op(const InterpArgs& A, Lane<kSmem>& L, const uint4 r) {
+template <int kM>
+__device__ __forceinline__ bool misc_op(const InterpArgs& A, Lane<kM>& L, const uint4 r) {
     switch (f_op(r)) {
     case GEVO_OP_SELECT: {
         const uint2 c = L.V(f_a(r));
@@ -898,8 +988,8 @@ __device__ __forceinline__ bool misc_op(const InterpArgs& A, Lane<kSmem>& L, con
 
 // run_to_barrier (vm.cpp:340-387) + step (389-482) for one simulated thread
 // from (th.block, th.ip). Returns kStopRet, kStopSync or kStopTrap.
-template <bool kSmem>
-__device__ int run_thread(const InterpArgs& A, Lane<kSmem>& L, Thread& th, const int64_t* s_cost,
+template <int kM>
+__device__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th, const int64_t* s_cost,
                           const volatile int32_t* first_fail) {
     Spin S;
     S.mode = 0;
@@ -989,7 +1079,19 @@ __device__ int run_thread(const InterpArgs& A, Lane<kSmem>& L, Thread& th, const
                 L.trap(GEVO_TRAP_UNKNOWN_BLOCK);
                 return kStopTrap;
             }
-            if (A.early_exit && --L.poll <= 0) {
+            if (Lane<kM>::kTP) {
+                // a lower simulated thread already stopped the instance
+                if (--L.poll <= 0) {
+                    L.poll = 16;
+                    if (*L.min_stop < L.tid)
+                        return kStopAbort;
+                    if (A.early_exit && (++L.poll2 & 127) == 0 &&
+                        first_fail[L.v] < static_cast<int32_t>(L.t)) {
+                        L.trap(GEVO_SKIPPED);
+                        return kStopTrap;
+                    }
+                }
+            } else if (A.early_exit && --L.poll <= 0) {
                 L.poll = 2048;
                 if (first_fail[L.v] < static_cast<int32_t>(L.t)) {
                     L.trap(GEVO_SKIPPED);
@@ -1028,15 +1130,15 @@ __device__ __forceinline__ uint32_t status_of(uint32_t code) {
                                        : GEVO_STATUS_TRAP;
 }
 
-template <bool kSmem>
-__device__ __forceinline__ void reset_values(Lane<kSmem>& L) {
+template <int kM>
+__device__ __forceinline__ void reset_values(Lane<kM>& L) {
     for (uint32_t s = 0; s < L.n_values; ++s)
         L.W(s, 0, GEVO_TAG_UNDEF);
 }
 
 // Machine::run for one instance (src/vm.cpp:114-150). Returns the status.
-template <bool kSmem>
-__device__ uint32_t run_instance(const InterpArgs& A, Lane<kSmem>& L, const gevo_variant& var,
+template <int kM>
+__device__ uint32_t run_instance(const InterpArgs& A, Lane<kM>& L, const gevo_variant& var,
                                  const int64_t* s_cost, const volatile int32_t* first_fail) {
     const int32_t T = A.threads;
     if (!(var.flags & GEVO_VAR_HAS_SYNC)) {
@@ -1132,8 +1234,8 @@ __device__ uint32_t run_instance(const InterpArgs& A, Lane<kSmem>& L, const gevo
 // 1.0 on any structural mismatch (resolved on the host per test), else the max
 // over oracle elements of the clamped relative difference. max() is exact and
 // order-free, so the per-buffer early return of the reference is not needed.
-template <bool kSmem>
-__device__ double instance_error(const InterpArgs& A, const Lane<kSmem>& L) {
+template <int kM>
+__device__ double instance_error(const InterpArgs& A, const Lane<kM>& L) {
     if (A.static_err[L.t])
         return 1.0;
     const uint32_t nt = static_cast<uint32_t>(A.n_tests);
@@ -1158,7 +1260,7 @@ __device__ double instance_error(const InterpArgs& A, const Lane<kSmem>& L) {
 
 } // namespace
 
-template <bool kSmem>
+template <int kM>
 __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ InterpArgs A) {
     __shared__ int64_t s_cost[GEVO_COST_CLASSES];
     if (threadIdx.x < GEVO_COST_CLASSES)
@@ -1176,11 +1278,13 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
     const uint32_t il = vl * nt + t;
     const uint64_t gi = static_cast<uint64_t>(v) * nt + t;
 
-    Lane<kSmem> L;
+    Lane<kM> L;
     L.v = v;
     L.t = t;
     L.il = il;
-    if (kSmem) {
+    L.sl = il;
+    L.seq = true;
+    if (Lane<kM>::kSmem) {
         L.gvf = nullptr;
         L.base = warp * A.row_lanes * A.max_slots + (lane & (A.row_lanes - 1));
         L.row = A.row_lanes;
@@ -1261,6 +1365,317 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
     rec.pad[1] = static_cast<uint8_t>(L.spin_dbg);
     A.rec[gi] = rec;
 
+    if (A.early_exit && status != GEVO_STATUS_SKIPPED &&
+        (status != GEVO_STATUS_COMPLETED || error > A.tolerance))
+        atomicMin(A.first_fail + v, static_cast<int32_t>(t));
+}
+
+// ---- thread-parallel lanes ---------------------------------------------------
+//
+// interp_tp_kernel gives every simulated thread of an instance its own lane:
+// a group of G lanes (G = threads rounded up to a power of two, <= 32) runs
+// one (variant, test) instance, 32 / G instances per warp, consecutive tests of
+// one variant side by side. A phase (the stretch between two barriers) runs
+// all threads at once instead of one after another; the instance's mutable
+// memory -- simulated shared words and its private copies of writable global
+// buffers -- lives in shared-memory cells {payload, tag | writer << 8 |
+// epoch << 16}.
+//
+// Exactness. Within a phase the reference runs threads in id order
+// (src/vm.cpp:121-142), so thread t sees every write of threads < t and none
+// of threads > t. Running them concurrently gives the same result whenever no
+// word is read by one thread and written by another in the same phase: every
+// read then returns the phase-start value or the reader's own write. Words
+// only written by several threads (nw-sync's s[80]) keep the value of the
+// highest writer -- each store is a compare-and-swap that never overwrites a
+// higher writer of the current epoch, and a thread's own stores land in
+// program order. Every lane records the words it read and wrote in per-phase
+// bitsets; at the phase end the group checks R_t & (W of any other thread);
+// any hit discards the parallel run and re-executes the whole instance with
+// threads in id order (plain stores), i.e. the reference schedule.
+//
+// Stops. The lowest thread id that traps (or exceeds its budget) decides the
+// record, as in the reference, where higher threads never run after it: the
+// cost and dynamic IR of threads above it in that phase are dropped, and those
+// lanes abandon their run early (min_stop poll). Barrier divergence is judged
+// on all threads once none trapped (vm.cpp:123-137).
+
+namespace {
+
+struct TpLayout {
+    uint32_t vf_words;     // uint2 entries of value files per CTA
+    uint32_t cell_words;   // uint2 cells per CTA
+    uint32_t bit_words;    // uint32 per bitset (R or W) per CTA
+};
+
+__device__ __forceinline__ TpLayout tp_layout(const InterpArgs& A, uint32_t warps) {
+    TpLayout l;
+    l.vf_words = warps * 32 * A.max_slots;
+    l.cell_words = warps * (32 / A.tp_group) * A.n_cells;
+    l.bit_words = warps * 32 * A.n_chunks;
+    return l;
+}
+
+template <typename T>
+__device__ __forceinline__ T group_sum(T x, uint32_t gmask, uint32_t G) {
+    for (uint32_t o = 1; o < G; o <<= 1)
+        x += __shfl_xor_sync(gmask, x, o, G);
+    return x;
+}
+
+// Conflict of the phase: some thread read a word another thread wrote.
+__device__ __forceinline__ bool group_conflict(const Lane<2>& L, uint32_t nch, uint32_t gmask,
+                                               uint32_t G) {
+    uint32_t hit = 0;
+    for (uint32_t k = 0; k < nch; ++k) {
+        const uint32_t w = L.wbits[k * L.bit_row], r = L.rbits[k * L.bit_row];
+        uint32_t a1 = w, a2 = 0; // written by >= 1 / >= 2 threads
+        for (uint32_t o = 1; o < G; o <<= 1) {
+            const uint32_t b1 = __shfl_xor_sync(gmask, a1, o, G);
+            const uint32_t b2 = __shfl_xor_sync(gmask, a2, o, G);
+            a2 |= b2 | (a1 & b1);
+            a1 |= b1;
+        }
+        hit |= r & (a2 | (a1 & ~w));
+    }
+    return __any_sync(gmask, hit != 0);
+}
+
+// (Re)initialises the instance: memory cells from the test's inputs, the
+// lane's value file, counters.
+__device__ __forceinline__ void tp_init_instance(const InterpArgs& A, Lane<2>& L, uint32_t tid,
+                                                 uint32_t G, uint32_t gmask) {
+    const uint32_t SW = static_cast<uint32_t>(max(A.shared_words, 0));
+    for (uint32_t w = tid; w < SW; w += G)
+        *L.cell(w) = make_uint2(0, GEVO_TAG_UNDEF);
+    const size_t tp0 = static_cast<size_t>(L.t) * A.n_params;
+    for (uint64_t m = L.writable; m; m &= m - 1) {
+        const uint32_t p = static_cast<uint32_t>(__ffsll(static_cast<long long>(m)) - 1);
+        const int32_t rows = A.buf_size[tp0 + p];
+        const uint32_t elem = A.buf_elem[tp0 + p];
+        for (int32_t e = static_cast<int32_t>(tid); e < rows; e += static_cast<int32_t>(G))
+            *L.cell(A.cell_off[p] + static_cast<uint32_t>(e)) = make_uint2(
+                __ldg(A.pool + A.pool_off[p] + static_cast<size_t>(e) * A.n_tests + L.t), elem);
+    }
+    for (uint32_t s = 0; s < L.n_values; ++s)
+        L.W(s, 0, GEVO_TAG_UNDEF);
+    L.cost = 0;
+    L.ir = 0;
+    L.code_out = GEVO_OK;
+    L.aux = 0;
+    __syncwarp(gmask);
+}
+
+} // namespace
+
+__global__ void __launch_bounds__(128) interp_tp_kernel(const __grid_constant__ InterpArgs A) {
+    __shared__ int64_t s_cost[GEVO_COST_CLASSES];
+    if (threadIdx.x < GEVO_COST_CLASSES)
+        s_cost[threadIdx.x] = A.cost[threadIdx.x];
+    __syncthreads();
+
+    const uint32_t warps = blockDim.x >> 5;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t G = A.tp_group, gpw = 32 / G;
+    const uint32_t tid = lane & (G - 1);
+    const uint32_t gbase = lane & ~(G - 1);
+    const uint32_t gmask = G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1) << gbase);
+    const uint32_t ic = warp * gpw + lane / G;            // instance within the CTA
+    const uint32_t inst = blockIdx.x * warps * gpw + ic;  // instance within the launch
+    if (inst >= A.n_inst)
+        return; // whole group
+    const uint32_t nt = static_cast<uint32_t>(A.n_tests);
+    const uint32_t vl = inst / nt, t = inst % nt;
+    const uint32_t v = A.v_begin + vl;
+    const uint64_t gi = static_cast<uint64_t>(v) * nt + t;
+    const bool active = tid < static_cast<uint32_t>(A.threads);
+    const uint32_t amask = __ballot_sync(gmask, active) >> gbase; // group-relative
+
+    const TpLayout lay = tp_layout(A, warps);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(g_vfs + lay.vf_words + lay.cell_words);
+    int32_t* s_min_stop = reinterpret_cast<int32_t*>(bits + 2 * lay.bit_words);
+
+    Lane<2> L;
+    L.gvf = nullptr;
+    L.base = warp * 32 * A.max_slots + lane;
+    L.row = 32;
+    L.v = v;
+    L.t = t;
+    L.il = inst;
+    L.sl = inst * G + tid;
+    L.tid = static_cast<int32_t>(tid);
+    L.cells = g_vfs + lay.vf_words + ic;
+    L.cell_row = warps * gpw;
+    L.rbits = bits + threadIdx.x;
+    L.wbits = bits + lay.bit_words + threadIdx.x;
+    L.bit_row = blockDim.x;
+    L.epoch = 0;
+    L.seq = false;
+    L.min_stop = s_min_stop + ic;
+    L.cost = 0;
+    L.ir = 0;
+    L.poll = 16;
+    L.poll2 = 0;
+    L.jumps = 0;
+    L.spin_dbg = 0;
+    L.code_out = GEVO_OK;
+    L.aux = 0;
+    L.writable = 0;
+
+    const volatile int32_t* first_fail = A.first_fail;
+    uint32_t status = GEVO_STATUS_TRAP;
+    double error = -1.0;
+    int64_t cost_total = 0, ir_total = 0;
+    const uint8_t setup = A.setup_code[t];
+    if (A.early_exit && first_fail[v] < static_cast<int32_t>(t)) {
+        L.code_out = GEVO_SKIPPED;
+        status = GEVO_STATUS_SKIPPED;
+    } else if (setup != GEVO_OK) {
+        L.code_out = setup;
+        L.aux = A.setup_aux[t];
+        status = GEVO_STATUS_TRAP;
+    } else {
+        const gevo_variant var = A.variants[v];
+        const uint32_t P = static_cast<uint32_t>(A.n_params);
+        L.code = A.insts + var.inst_base;
+        L.dblk = A.dblocks + var.block_base;
+        L.arm = A.arms + var.arm_base;
+        L.n_values = var.n_values;
+        L.n_slots = var.n_slots;
+        L.writable = var.writable;
+        const uint32_t lit_begin = var.n_values + P + 2;
+        L.stage_base = lit_begin + var.n_lits;
+        const size_t tp0 = static_cast<size_t>(t) * P;
+        for (uint32_t p = 0; p < P; ++p)
+            L.W(var.n_values + p, A.param_payload[tp0 + p], A.param_tag[tp0 + p]);
+        L.W(var.n_values + P, 0, GEVO_TAG_POISON_PARAM);
+        L.W(var.n_values + P + 1, 0, GEVO_TAG_POISON_MISSING);
+        for (uint32_t k = 0; k < var.n_lits; ++k)
+            L.W(lit_begin + k, __ldg(A.lit_payload + var.lit_base + k),
+                __ldg(A.lit_tag + var.lit_base + k));
+        tp_init_instance(A, L, tid, G, gmask);
+
+        Thread th{0, 0, -1, 0, 0, false};
+        int64_t cost_commit = 0, ir_commit = 0;
+        for (;;) { // phases
+            ++L.epoch;
+            if (!L.seq) {
+                for (uint32_t k = 0; k < A.n_chunks; ++k) {
+                    L.rbits[k * L.bit_row] = 0;
+                    L.wbits[k * L.bit_row] = 0;
+                }
+            }
+            if (tid == 0)
+                *const_cast<int32_t*>(L.min_stop) = INT32_MAX;
+            __syncwarp(gmask);
+            int kind = kStopIdle;
+            bool restart = false;
+            if (!L.seq) {
+                if (active) {
+                    kind = run_thread(A, L, th, s_cost, first_fail);
+                    if (kind == kStopTrap)
+                        atomicMin(const_cast<int32_t*>(L.min_stop), L.tid);
+                }
+                __syncwarp(gmask);
+                restart = L.epoch >= 0xFFFFu || group_conflict(L, A.n_chunks, gmask, G);
+            } else {
+                for (uint32_t u = 0; u < static_cast<uint32_t>(A.threads); ++u) {
+                    if (tid == u)
+                        kind = run_thread(A, L, th, s_cost, first_fail);
+                    if (__shfl_sync(gmask, kind, u, G) == kStopTrap)
+                        break;
+                }
+            }
+            if (restart) {
+                // reference schedule from the start: threads in id order
+                if (A.counters && tid == 0)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 2), 1ull);
+                L.seq = true;
+                L.epoch = 0;
+                th = Thread{0, 0, -1, 0, 0, false};
+                cost_commit = ir_commit = 0;
+                __syncwarp(gmask);
+                tp_init_instance(A, L, tid, G, gmask);
+                continue;
+            }
+            const uint32_t traps = (__ballot_sync(gmask, kind == kStopTrap) >> gbase) & amask;
+            if (traps) {
+                const uint32_t ts = __ffs(traps) - 1;
+                const bool mine = tid <= ts;
+                cost_total = group_sum<long long>(mine ? L.cost : cost_commit, gmask, G);
+                ir_total = group_sum<long long>(mine ? L.ir : ir_commit, gmask, G);
+                L.code_out = __shfl_sync(gmask, L.code_out, ts, G);
+                L.aux = __shfl_sync(gmask, L.aux, ts, G);
+                status = L.code_out == GEVO_BUDGET_EXCEEDED ? GEVO_STATUS_BUDGET
+                         : L.code_out == GEVO_SKIPPED      ? GEVO_STATUS_SKIPPED
+                                                           : GEVO_STATUS_TRAP;
+                break;
+            }
+            cost_total = group_sum<long long>(L.cost, gmask, G);
+            ir_total = group_sum<long long>(L.ir, gmask, G);
+            const uint32_t rets = (__ballot_sync(gmask, kind == kStopRet) >> gbase) & amask;
+            if (rets == amask) {
+                status = GEVO_STATUS_COMPLETED;
+                break;
+            }
+            const uint32_t bar0 = __shfl_sync(gmask, th.bar, 0, G);
+            const uint32_t same =
+                (__ballot_sync(gmask, kind == kStopSync && th.bar == bar0) >> gbase) & amask;
+            if (same != amask) {
+                L.code_out = GEVO_TRAP_DIVERGENCE;
+                L.aux = 0;
+                status = GEVO_STATUS_TRAP;
+                break;
+            }
+            ++th.ip; // step past the barrier
+            cost_commit = L.cost;
+            ir_commit = L.ir;
+        }
+        if (status == GEVO_STATUS_COMPLETED) {
+            // compute_error (src/vm.cpp:536-556): max over oracle elements,
+            // spread over the group's lanes (max is order-free).
+            double worst = 0.0;
+            if (A.static_err[t]) {
+                worst = 1.0;
+            } else {
+                for (int32_t e = A.entry_begin[t]; e < A.entry_begin[t + 1]; ++e) {
+                    const OracleEntryDev en = A.entries[e];
+                    const uint32_t p = static_cast<uint32_t>(en.param);
+                    const bool priv = (L.writable >> p) & 1ull;
+                    for (int32_t k = static_cast<int32_t>(tid); k < en.size;
+                         k += static_cast<int32_t>(G)) {
+                        const uint32_t cw =
+                            priv ? L.cell(A.cell_off[p] + static_cast<uint32_t>(k))->x
+                                 : __ldg(A.pool + A.pool_off[p] + static_cast<size_t>(k) * nt + t);
+                        const uint32_t ow = __ldg(A.pool + en.off + static_cast<size_t>(k) * nt + t);
+                        const double d =
+                            rel_diff(word_to_double(cw, en.elem), word_to_double(ow, en.elem));
+                        worst = (worst < d) ? d : worst;
+                    }
+                }
+                for (uint32_t o = 1; o < G; o <<= 1) {
+                    const double x = __shfl_xor_sync(gmask, worst, o, G);
+                    worst = (worst < x) ? x : worst;
+                }
+            }
+            error = worst;
+        }
+    }
+    const uint32_t jumps = group_sum<uint32_t>(L.jumps, gmask, G);
+    if (tid != 0)
+        return;
+    gevo_test_record rec;
+    rec.cost = cost_total;
+    rec.ir = ir_total;
+    rec.error = error;
+    rec.aux = L.aux;
+    rec.status = static_cast<uint8_t>(status);
+    rec.code = static_cast<uint8_t>(L.code_out);
+    rec.pad[0] = static_cast<uint8_t>(min(jumps, 255u));
+    rec.pad[1] = static_cast<uint8_t>(L.seq ? 1 : 0);
+    A.rec[gi] = rec;
+    if (A.counters)
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3), 1ull);
     if (A.early_exit && status != GEVO_STATUS_SKIPPED &&
         (status != GEVO_STATUS_COMPLETED || error > A.tolerance))
         atomicMin(A.first_fail + v, static_cast<int32_t>(t));
@@ -1403,14 +1818,45 @@ cudaError_t launch_interp(const InterpArgs& A, cudaStream_t stream) {
     const uint64_t warps = static_cast<uint64_t>(A.n_var) * A.warps_per_variant;
     const unsigned grid = static_cast<unsigned>((warps + s.warps_per_cta - 1) / s.warps_per_cta);
     if (s.vf_global) {
-        interp_kernel<false><<<grid, 32 * s.warps_per_cta, 0, stream>>>(A);
+        interp_kernel<0><<<grid, 32 * s.warps_per_cta, 0, stream>>>(A);
         return cudaGetLastError();
     }
     const cudaError_t e = cudaFuncSetAttribute(
-        interp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s.smem));
+        interp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s.smem));
     if (e != cudaSuccess)
         return e;
-    interp_kernel<true><<<grid, 32 * s.warps_per_cta, s.smem, stream>>>(A);
+    interp_kernel<1><<<grid, 32 * s.warps_per_cta, s.smem, stream>>>(A);
+    return cudaGetLastError();
+}
+
+TpShape tp_shape(uint32_t group, uint32_t max_slots, uint32_t n_cells, uint32_t n_chunks) {
+    TpShape s{0, 0};
+    for (uint32_t w = 4; w >= 1; w >>= 1) {
+        const size_t inst = static_cast<size_t>(w) * (32 / group);
+        const size_t bytes = static_cast<size_t>(w) * 32 * max_slots * 8 + inst * n_cells * 8 +
+                             2 * static_cast<size_t>(w) * 32 * n_chunks * 4 + inst * 4;
+        if (bytes <= kSmemBudget) {
+            s.warps_per_cta = w;
+            s.smem = bytes;
+            return s;
+        }
+    }
+    return s;
+}
+
+cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream) {
+    if (A.n_inst == 0)
+        return cudaSuccess;
+    const TpShape s = tp_shape(A.tp_group, A.max_slots, A.n_cells, A.n_chunks);
+    if (s.warps_per_cta == 0)
+        return cudaErrorInvalidConfiguration;
+    const uint64_t per_cta = static_cast<uint64_t>(s.warps_per_cta) * (32 / A.tp_group);
+    const unsigned grid = static_cast<unsigned>((A.n_inst + per_cta - 1) / per_cta);
+    const cudaError_t e = cudaFuncSetAttribute(
+        interp_tp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s.smem));
+    if (e != cudaSuccess)
+        return e;
+    interp_tp_kernel<<<grid, 32 * s.warps_per_cta, s.smem, stream>>>(A);
     return cudaGetLastError();
 }
 

@@ -85,12 +85,20 @@ struct InterpArgs {
     uint32_t* sp_log;               // [kSpinLog][inst] x 3: store-log key, old payload, old tag|flags
     uint32_t* sp_ld;                // [kSpinLog][inst] load-log keys
     int64_t spin_threshold;         // per-thread executed count that arms it
+    uint32_t n_spin;                // spin scratch columns (instances, or lanes for tp)
+
+    // thread-parallel lanes (interp_tp_kernel)
+    uint32_t tp_group;              // lanes per instance (pow2 >= threads, <= 32)
+    uint32_t n_cells;               // memory cells per instance: shared words + writable rows
+    uint32_t n_chunks;              // 32-bit chunks of a per-lane read / write bitset
+    uint32_t cell_off[GEVO_MAX_PARAMS]; // first cell of writable global param p
 
     // outputs
     gevo_test_record* rec;          // [variant * n_tests + test]
     int32_t* first_fail;            // [variant] (early-exit mode)
     int32_t early_exit;
-    uint64_t* counters;             // [2]: accelerated spins, jumped instructions (nullable)
+    uint64_t* counters;             // [4]: accelerated spins, jumped instructions,
+                                    // tp instances re-run in id order, tp instances (nullable)
 };
 
 // Memory words one abstract iterate may store to / load from.
@@ -116,6 +124,15 @@ cudaError_t launch_block_cost(const gevo_block* blocks, const gevo_inst* insts,
                               const gevo_variant* variants, uint32_t n_variants,
                               const int64_t* cost_table, uint4* out, cudaStream_t stream);
 cudaError_t launch_interp(const InterpArgs& A, cudaStream_t stream);
+
+// Thread-parallel launch shape: warps per CTA and dynamic shared memory, or
+// warps_per_cta == 0 when the instance state does not fit on chip.
+struct TpShape {
+    uint32_t warps_per_cta;
+    size_t smem;
+};
+TpShape tp_shape(uint32_t group, uint32_t max_slots, uint32_t n_cells, uint32_t n_chunks);
+cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream);
 cudaError_t launch_error(const uint32_t* cand, const uint32_t* orc, const uint8_t* elem, uint32_t n,
                          double* out, cudaStream_t stream);
 cudaError_t launch_fitness(const gevo_test_record* rec, uint32_t n_variants, int32_t n_tests,

@@ -232,6 +232,36 @@ int64_t spin_threshold() {
     return v;
 }
 
+// GEVO_TP=0 forces the sequential-lane interpreter.
+bool tp_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("GEVO_TP");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
+// Spin-accelerator scratch for `cols` columns (instances or lanes).
+void reserve_spin(DeviceImpl& dev, gevo::InterpArgs& A, size_t cols) {
+    const size_t n = cols * A.max_slots;
+    dev.sp_base.reserve(n * 4);
+    dev.sp_btag.reserve(n);
+    dev.sp_delta.reserve(n * 4);
+    dev.sp_cur.reserve(n * 4);
+    dev.sp_hvary.reserve(n);
+    dev.sp_cvary.reserve(n);
+    dev.sp_log.reserve(cols * gevo::kSpinLog * 3 * 4);
+    dev.sp_ld.reserve(cols * gevo::kSpinLog * 4);
+    A.sp_hvary = dev.sp_hvary.as<uint8_t>();
+    A.sp_cvary = dev.sp_cvary.as<uint8_t>();
+    A.sp_log = dev.sp_log.as<uint32_t>();
+    A.sp_ld = dev.sp_ld.as<uint32_t>();
+    A.sp_base = dev.sp_base.as<uint32_t>();
+    A.sp_btag = dev.sp_btag.as<uint8_t>();
+    A.sp_delta = dev.sp_delta.as<uint32_t>();
+    A.sp_cur = dev.sp_cur.as<uint32_t>();
+}
+
 // Launches the interpreter over all variants in scratch-bounded chunks, then
 // the per-variant reduction. Records land in dev.rec / dev.vrec.
 int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const gevo_batch_header& h,
@@ -259,6 +289,56 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
           "block_cost_kernel launch");
     ++launches;
     A.dblocks = dev.bcost.as<uint4>();
+
+    const int64_t thr = spin_threshold();
+    if (!dev.counters.ptr) {
+        dev.counters.reserve(32);
+        check(cudaMemsetAsync(dev.counters.ptr, 0, 32, s), "counters");
+    }
+    A.counters = dev.counters.as<uint64_t>();
+
+    // Thread-parallel lanes (one lane per simulated thread) whenever the
+    // instance state fits on chip; the sequential-lane kernel otherwise.
+    uint32_t group = 1;
+    while (group < static_cast<uint32_t>(std::max(ex.threads, 1)))
+        group <<= 1;
+    uint32_t n_cells = static_cast<uint32_t>(std::max(ex.shared_words, 0));
+    for (int p = 0; p < S.n_params; ++p) {
+        A.cell_off[p] = n_cells;
+        if ((writable_any >> p) & 1ull)
+            n_cells += static_cast<uint32_t>(S.pool_rows[static_cast<size_t>(p)]);
+    }
+    const uint32_t n_chunks = std::max<uint32_t>((n_cells + 31) / 32, 1);
+    const gevo::TpShape tps = gevo::tp_shape(group, A.max_slots, n_cells, n_chunks);
+    if (ex.threads >= 1 && ex.threads <= 32 && !opt.want_outputs && !opt.sequential &&
+        tps.warps_per_cta > 0 && tp_enabled()) {
+        A.tp_group = group;
+        A.n_cells = n_cells;
+        A.n_chunks = n_chunks;
+        const size_t per_lane = thr > 0 ? 15 * static_cast<size_t>(A.max_slots) + 16 * gevo::kSpinLog
+                                        : 0;
+        size_t chunk = std::max<size_t>(dev.scratch_budget / (std::max<size_t>(per_lane, 1) * group * T),
+                                        64);
+        chunk = std::min<size_t>(chunk, std::max<uint32_t>(h.n_variants, 1));
+        const size_t lanes = chunk * T * group;
+        if (thr > 0) {
+            reserve_spin(dev, A, lanes);
+            A.spin_threshold = thr;
+        }
+        for (uint64_t vb = 0; vb < h.n_variants; vb += chunk) {
+            gevo::InterpArgs L = A;
+            L.v_begin = static_cast<uint32_t>(vb);
+            L.n_var = static_cast<uint32_t>(std::min<uint64_t>(chunk, h.n_variants - vb));
+            L.n_inst = L.n_var * T;
+            L.n_spin = L.n_inst * group;
+            check(gevo::launch_interp_tp(L, s), "interp_tp_kernel launch");
+            ++launches;
+        }
+        check(gevo::launch_fitness(dev.rec.as<gevo_test_record>(), h.n_variants, S.n_tests,
+                                   opt.tolerance, dev.vrec.as<gevo_variant_record>(), s),
+              "fitness_kernel launch");
+        return launches + 1;
+    }
 
     const gevo::LaunchShape shape = gevo::interp_shape(S.n_tests, A.max_slots);
     A.row_lanes = shape.row_lanes;
@@ -303,37 +383,16 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
         dev.vf.reserve(cap * A.max_slots * 8);
         A.vf = dev.vf.as<uint2>();
     }
-    const int64_t thr = spin_threshold();
     if (thr > 0) {
-        const size_t n = cap * A.max_slots;
-        dev.sp_base.reserve(n * 4);
-        dev.sp_btag.reserve(n);
-        dev.sp_delta.reserve(n * 4);
-        dev.sp_cur.reserve(n * 4);
-        dev.sp_hvary.reserve(n);
-        dev.sp_cvary.reserve(n);
-        dev.sp_log.reserve(cap * gevo::kSpinLog * 3 * 4);
-        dev.sp_ld.reserve(cap * gevo::kSpinLog * 4);
-        A.sp_hvary = dev.sp_hvary.as<uint8_t>();
-        A.sp_cvary = dev.sp_cvary.as<uint8_t>();
-        A.sp_log = dev.sp_log.as<uint32_t>();
-        A.sp_ld = dev.sp_ld.as<uint32_t>();
-        A.sp_base = dev.sp_base.as<uint32_t>();
-        A.sp_btag = dev.sp_btag.as<uint8_t>();
-        A.sp_delta = dev.sp_delta.as<uint32_t>();
-        A.sp_cur = dev.sp_cur.as<uint32_t>();
+        reserve_spin(dev, A, cap);
         A.spin_threshold = thr;
     }
-    if (!dev.counters.ptr) {
-        dev.counters.reserve(16);
-        check(cudaMemsetAsync(dev.counters.ptr, 0, 16, s), "counters");
-    }
-    A.counters = dev.counters.as<uint64_t>();
     for (uint64_t vb = 0; vb < h.n_variants; vb += chunk) {
         gevo::InterpArgs L = A;
         L.v_begin = static_cast<uint32_t>(vb);
         L.n_var = static_cast<uint32_t>(std::min<uint64_t>(chunk, h.n_variants - vb));
         L.n_inst = L.n_var * T;
+        L.n_spin = L.n_inst;
         size_t words = 0;
         for (int p = 0; p < S.n_params; ++p) {
             L.priv_off[p] = words * L.n_inst;
@@ -519,18 +578,25 @@ float evaluate_resident(ResidentBatch& rb, const ExecImage& exec, const EvalOpti
     return ms;
 }
 
-void spin_counters(Device& devh, uint64_t out[2], bool reset) {
+namespace {
+void read_counters(Device& devh, uint64_t out[2], bool reset, size_t first) {
     std::lock_guard<std::mutex> g(devh.lock());
     DeviceImpl& dev = devh.impl();
     out[0] = out[1] = 0;
     if (!dev.counters.ptr)
         return;
     check(cudaSetDevice(dev.ordinal), "cudaSetDevice");
-    check(cudaMemcpyAsync(out, dev.counters.ptr, 16, cudaMemcpyDeviceToHost, dev.stream), "counters");
+    uint64_t* c = dev.counters.as<uint64_t>() + first;
+    check(cudaMemcpyAsync(out, c, 16, cudaMemcpyDeviceToHost, dev.stream), "counters");
     if (reset)
-        check(cudaMemsetAsync(dev.counters.ptr, 0, 16, dev.stream), "counters");
+        check(cudaMemsetAsync(c, 0, 16, dev.stream), "counters");
     check(cudaStreamSynchronize(dev.stream), "counters");
 }
+} // namespace
+
+void spin_counters(Device& devh, uint64_t out[2], bool reset) { read_counters(devh, out, reset, 0); }
+
+void tp_counters(Device& devh, uint64_t out[2], bool reset) { read_counters(devh, out, reset, 2); }
 
 ParetoRank rank_on_device(Device& devh, const std::vector<FitnessVector>& fits, bool single_group) {
     ParetoRank r;

@@ -57,6 +57,7 @@ struct EvalOptions {
     bool early_exit = false;      // skip tests after a variant's first failure
     bool want_tests = false;      // copy per-test records back
     bool want_outputs = false;    // copy final global buffers back (small batches)
+    bool sequential = false;      // force the sequential-lane interpreter
 };
 
 struct EvalResult {
@@ -86,6 +87,9 @@ float evaluate_resident(ResidentBatch& rb, const ExecImage& exec, const EvalOpti
 
 // Spin-accelerator counters of a device: {loops jumped, instructions skipped}.
 void spin_counters(Device& dev, uint64_t out[2], bool reset);
+// Thread-parallel interpreter counters: {instances re-run in thread-id order
+// after a same-phase cross-thread conflict, instances run}.
+void tp_counters(Device& dev, uint64_t out[2], bool reset);
 
 // GPU NSGA ranking (front + crowding + fronts in reference order).
 ParetoRank rank_on_device(Device& dev, const std::vector<FitnessVector>& fits, bool single_group);

@@ -16,17 +16,29 @@ for bench in BENCHES:
     cands = gevo.sample_candidates(bench, 1024, 1, 4)
     suite = gevo.Suite.from_benchmark(bench, 16, gevo.train_seed(1))
     cfg = suite.exec_config()
-    times = []
+    times, seq_times, reruns = [], [], []
     for i, c in enumerate(cands):
         b = suite.batch()
         b.add_patch(c)
-        b.make_resident()
-        b.eval_resident(cfg, early_exit=True)
-        _, st = b.eval_resident(cfg, early_exit=True)
+        b.eval(cfg, early_exit=True)
+        gevo.tp_counters(reset=True)
+        _, _, st = b.eval(cfg, early_exit=True)
+        reruns.append(gevo.tp_counters(reset=True)[0])
         times.append((st.device_ms, i))
+        _, _, st = b.eval(cfg, early_exit=True, sequential=True)
+        seq_times.append(st.device_ms)
+    # one empty-ish batch: launch overhead floor
+    b = suite.batch()
+    b.add_ir(gevo.benchmark_ir(bench))
+    b.eval(cfg, early_exit=True)
+    _, _, st0 = b.eval(cfg, early_exit=True)
     times.sort(reverse=True)
     tot = sum(t for t, _ in times)
-    summary[bench] = {"sum_ms": tot, "top": [(round(t, 3), i) for t, i in times[:20]],
+    summary[bench] = {"sum_ms": tot, "seq_sum_ms": sum(seq_times), "original_ms": st0.device_ms,
+                      "median_ms": sorted(t for t, _ in times)[len(times) // 2],
+                      "seq_median_ms": sorted(seq_times)[len(seq_times) // 2],
+                      "variants_rerun": sum(1 for r in reruns if r),
+                      "top": [(round(t, 3), i, reruns[i]) for t, i in times[:20]],
                       "n_over_1ms": sum(1 for t, _ in times if t > 1.0)}
     print(bench, json.dumps(summary[bench]), flush=True)
     with open(os.path.join(ROOT, "gpurun_out", "tail_%s.txt" % bench), "w") as f:
