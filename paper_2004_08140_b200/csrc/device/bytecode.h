@@ -36,7 +36,10 @@ enum {
     GEVO_OP_BR, GEVO_OP_SYNC, GEVO_OP_RET,
     GEVO_OP_TID, GEVO_OP_NTHREADS,
     GEVO_OP_CONST,
-    GEVO_OP_COUNT
+    GEVO_OP_COUNT,
+    /* device-only: sentinel record after every block ("fell off the end of a
+       block", src/vm.cpp:345-346) */
+    GEVO_OP_FELL = GEVO_OP_COUNT
 };
 
 /* Cost classes: index into the 14-entry cost table (field order of
@@ -176,7 +179,7 @@ typedef struct {
 } gevo_batch_header;
 
 #define GEVO_MAGIC 0x4F564547u
-#define GEVO_VERSION 2u
+#define GEVO_VERSION 3u
 
 /* Per-(variant, test) record written by the interpreter. */
 typedef struct {

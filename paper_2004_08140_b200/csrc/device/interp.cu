@@ -110,15 +110,52 @@ __device__ __forceinline__ bool bad_tag(uint32_t t) {
     return t == GEVO_TAG_UNDEF || t == GEVO_TAG_POISON_PARAM || t == GEVO_TAG_POISON_MISSING;
 }
 
-// Value file of one lane: slot s lives at index base + s * row of the CTA's
-// shared array (kM >= 1) or of the global scratch array (kM == 0).
+// Explicit shared-memory accesses by 32-bit shared-window address: the
+// interpreter's value files and instance memory never go through generic
+// pointers (no per-access window conversion).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint2 lds2(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts2(uint32_t a, uint32_t x, uint32_t y) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ uint32_t lds1(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts1(uint32_t a, uint32_t x) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(x) : "memory");
+}
+__device__ __forceinline__ unsigned long long cas64(uint32_t a, unsigned long long cmp,
+                                                    unsigned long long val) {
+    unsigned long long old;
+    asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "r"(a), "l"(cmp), "l"(val)
+                 : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned long long lds64(uint32_t a) {
+    unsigned long long v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+
+// Value file of one lane: slot s lives at shared address vsh + s * vstr
+// (kM >= 1) or at index base + s * row of the global scratch array (kM == 0).
 // kM: 0 = sequential lanes, value file in global scratch; 1 = sequential
-// lanes, value file in shared memory; 2 = thread-parallel lanes (one lane per
-// simulated thread, instance memory in shared-memory cells, see interp_tp_kernel).
+// lanes, value file in shared memory; 2 = thread-parallel (one warp per
+// simulated thread, instance memory in shared-memory cells, interp_tp_kernel).
 template <int kM>
 struct Lane {
     static constexpr bool kSmem = kM >= 1;
     static constexpr bool kTP = kM == 2;
+    uint32_t vsh;    // kSmem: shared address of slot 0
+    uint32_t vstr;   // kSmem: bytes from one slot to the next
     uint2* gvf;      // global value file (kM == 0)
     uint32_t base;   // element index of slot 0
     uint32_t row;
@@ -134,15 +171,15 @@ struct Lane {
     uint32_t v, t, il;
     uint32_t sl;     // spin-accelerator scratch column (instance, or lane when kTP)
     int32_t tid;
-    // thread-parallel lanes (kTP)
-    uint2* cells;            // instance memory cells [word][cta instance] in shared memory
-    uint32_t cell_row;       // cta instances per word row
-    uint32_t* rbits;         // read / write bitsets of this lane: chunk k at [k * bit_row]
-    uint32_t* wbits;
-    uint32_t bit_row;
+    const uint32_t* binfo;   // [param] size << 8 | elem of this lane's test
+    // thread-parallel (kTP)
+    uint32_t csh;            // shared address of memory cell 0 of the instance
+    uint32_t cstr;           // bytes from one cell to the next
+    uint32_t rsh, wsh;       // shared addresses of this lane's read / write bitset chunk 0
+    uint32_t bstr;           // bytes from one bitset chunk to the next
+    uint32_t msh;            // shared address of the instance's min_stop
     uint32_t epoch;          // phase number (max-tid-wins store rule)
     bool seq;                // sequential fallback: plain stores, no conflict tracking
-    const volatile int32_t* min_stop; // lowest tid of the instance that stopped this phase
     // counters
     int64_t cost;
     int64_t ir;
@@ -156,17 +193,17 @@ struct Lane {
 
     __device__ __forceinline__ uint2 V(uint32_t s) const {
         if (kSmem)
-            return g_vfs[base + s * row];
+            return lds2(vsh + s * vstr);
         return gvf[base + s * row];
     }
     __device__ __forceinline__ void W(uint32_t s, uint32_t payload, uint32_t tag) {
         if (kSmem)
-            g_vfs[base + s * row] = make_uint2(payload, tag);
+            sts2(vsh + s * vstr, payload, tag);
         else
             gvf[base + s * row] = make_uint2(payload, tag);
     }
-    // kTP: memory cell of word w of the instance
-    __device__ __forceinline__ uint2* cell(uint32_t w) const { return cells + w * cell_row; }
+    // kTP: shared address of memory cell w of the instance
+    __device__ __forceinline__ uint32_t cell(uint32_t w) const { return csh + w * cstr; }
 
     __device__ __forceinline__ bool trap(uint32_t c, int32_t x = 0) {
         code_out = c;
@@ -249,22 +286,21 @@ struct Spin {
 };
 
 template <int kM>
-__device__ __forceinline__ int64_t suffix_cost(const Lane<kM>& L, const Blk& b, uint32_t from,
-                                               const int64_t* s_cost) {
+__device__ __noinline__ int64_t suffix_cost(const InterpArgs& A, const Lane<kM>& L, const Blk& b,
+                                            uint32_t from) {
     int64_t c = 0;
     for (uint32_t j = from; j < b.len; ++j)
-        c += s_cost[__ldg(reinterpret_cast<const uint32_t*>(L.code + b.start + j)) >> 24];
+        c += A.cost[__ldg(reinterpret_cast<const uint32_t*>(L.code + b.start + j)) >> 24];
     return c;
 }
 
 // Charges instructions [from, len) of the current block on entry / resume.
 template <int kM>
 __device__ __forceinline__ void charge_block(const InterpArgs& A, Lane<kM>& L, Thread& th,
-                                             const Blk& b, int64_t bcost, uint32_t from,
-                                             const int64_t* s_cost) {
+                                             const Blk& b, int64_t bcost, uint32_t from) {
     const int64_t n = static_cast<int64_t>(b.len) - from;
     if (th.executed + n <= A.budget) {
-        L.cost += from == 0 ? bcost : suffix_cost(L, b, from, s_cost);
+        L.cost += from == 0 ? bcost : suffix_cost(A, L, b, from);
         L.ir += n;
         th.executed += n;
         th.slow = false;
@@ -275,12 +311,12 @@ __device__ __forceinline__ void charge_block(const InterpArgs& A, Lane<kM>& L, T
 
 // Refunds instructions [from, len) charged on entry that will not run.
 template <int kM>
-__device__ __forceinline__ void refund(Lane<kM>& L, Thread& th, const Blk& b, uint32_t from,
-                                       const int64_t* s_cost) {
+__device__ __forceinline__ void refund(const InterpArgs& A, Lane<kM>& L, Thread& th, const Blk& b,
+                                       uint32_t from) {
     if (th.slow || from >= b.len)
         return;
     const int64_t n = static_cast<int64_t>(b.len) - from;
-    L.cost -= suffix_cost(L, b, from, s_cost);
+    L.cost -= suffix_cost(A, L, b, from);
     L.ir -= n;
     th.executed -= n;
 }
@@ -288,8 +324,8 @@ __device__ __forceinline__ void refund(Lane<kM>& L, Thread& th, const Blk& b, ui
 // Per-instruction charge (exact mode): cost and budget before any effect.
 template <int kM>
 __device__ __forceinline__ bool charge_one(const InterpArgs& A, Lane<kM>& L, Thread& th,
-                                           uint32_t cls, const int64_t* s_cost) {
-    L.cost += s_cost[cls];
+                                           uint32_t cls) {
+    L.cost += A.cost[cls];
     ++L.ir;
     if (++th.executed > A.budget)
         return L.trap(GEVO_BUDGET_EXCEEDED);
@@ -406,7 +442,7 @@ template <int kM>
 __device__ __forceinline__ uint2 mem_word(const InterpArgs& A, const Lane<kM>& L, uint32_t key) {
     const uint32_t eff = key & 0xFFFFFF, space = key >> 24;
     if (Lane<kM>::kTP) {
-        const uint2 c = *L.cell(space == 0x80 ? eff : A.cell_off[space - 1] + eff);
+        const uint2 c = lds2(L.cell(space == 0x80 ? eff : A.cell_off[space - 1] + eff));
         return make_uint2(c.x, c.y & 0xFF);
     }
     if (space == 0x80) {
@@ -750,14 +786,14 @@ __device__ __forceinline__ bool phi_arm(const Lane<kM>& L, const uint4 r, int32_
 
 // enter_block (vm.cpp:293-333): charge and stage every leading phi, then write.
 template <int kM>
-__device__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Thread& th, const int64_t* s_cost,
+__device__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Thread& th,
                             int32_t target, Blk& b, Spin& S) {
     th.prev = th.block;
     th.block = target;
     th.ip = 0;
     int64_t bcost;
     b = load_blk(L.dblk, target, bcost);
-    charge_block(A, L, th, b, bcost, 0, s_cost);
+    charge_block(A, L, th, b, bcost, 0);
     const uint32_t n = b.nphi;
     if (n == 0)
         return true;
@@ -765,21 +801,21 @@ __device__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Thread& th, const 
     if (n == 1) {
         // a single phi reads nothing another phi writes: no staging needed
         const uint4 r = fetch_inst(L.code, b.start);
-        if (th.slow && !charge_one(A, L, th, f_cls(r), s_cost))
+        if (th.slow && !charge_one(A, L, th, f_cls(r)))
             return false;
         uint32_t ref;
         if (!phi_arm(L, r, th.prev, ref)) {
-            refund(L, th, b, 1, s_cost);
+            refund(A, L, th, b, 1);
             return L.trap(GEVO_TRAP_PHI_NO_INCOMING);
         }
         uint2 v;
         if (!L.fetch(ref, v)) {
-            refund(L, th, b, 1, s_cost);
+            refund(A, L, th, b, 1);
             return false;
         }
         th.ip = 1;
         if (!L.set(f_res(r), v.x, v.y)) {
-            refund(L, th, b, 1, s_cost);
+            refund(A, L, th, b, 1);
             return false;
         }
         if (track)
@@ -788,16 +824,16 @@ __device__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Thread& th, const 
     }
     for (uint32_t j = 0; j < n; ++j) {
         const uint4 r = fetch_inst(L.code, b.start + j);
-        if (th.slow && !charge_one(A, L, th, f_cls(r), s_cost))
+        if (th.slow && !charge_one(A, L, th, f_cls(r)))
             return false;
         uint32_t ref;
         if (!phi_arm(L, r, th.prev, ref)) {
-            refund(L, th, b, j + 1, s_cost);
+            refund(A, L, th, b, j + 1);
             return L.trap(GEVO_TRAP_PHI_NO_INCOMING);
         }
         uint2 v;
         if (!L.fetch(ref, v)) {
-            refund(L, th, b, j + 1, s_cost);
+            refund(A, L, th, b, j + 1);
             return false;
         }
         L.W(L.stage_base + j, v.x, v.y);
@@ -809,7 +845,7 @@ __device__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Thread& th, const 
         const uint4 r = fetch_inst(L.code, b.start + j);
         const uint2 v = L.V(L.stage_base + j);
         if (!L.set(f_res(r), v.x, v.y)) {
-            refund(L, th, b, n, s_cost);
+            refund(A, L, th, b, n);
             return false;
         }
         if (track)
@@ -849,10 +885,10 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
             w = static_cast<uint32_t>(eff);
         } else {
             const uint32_t prm = p.y & 0x3F;
-            const size_t tp = static_cast<size_t>(L.t) * A.n_params + prm;
-            if (eff < 0 || eff >= __ldg(A.buf_size + tp))
+            const uint32_t info = __ldg(L.binfo + prm);
+            if (eff < 0 || eff >= static_cast<int32_t>(info >> 8))
                 return L.trap(GEVO_TRAP_GLOBAL_OOB);
-            const uint32_t elem = __ldg(A.buf_elem + tp);
+            const uint32_t elem = info & 0xFF;
             if (op == GEVO_OP_LOAD) {
                 if (elem != f_aux(r))
                     return L.trap(GEVO_TRAP_GLOBAL_LOAD_TYPE);
@@ -868,12 +904,14 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
             }
             w = A.cell_off[prm] + static_cast<uint32_t>(eff);
         }
-        uint2* c = L.cell(w);
+        const uint32_t ca = L.cell(w);
         const uint32_t bit = 1u << (w & 31);
         if (op == GEVO_OP_LOAD) {
-            if (!L.seq)
-                L.rbits[(w >> 5) * L.bit_row] |= bit;
-            const uint2 x = *c;
+            if (!L.seq) {
+                const uint32_t ba = L.rsh + (w >> 5) * L.bstr;
+                sts1(ba, lds1(ba) | bit);
+            }
+            const uint2 x = lds2(ca);
             if (p.y == GEVO_TAG_PTR_SHARED) {
                 const uint32_t wt = x.y & 0xFF;
                 if (wt == GEVO_TAG_UNDEF)
@@ -884,24 +922,25 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
             return L.set(f_res(r), x.x, x.y & 0xFF);
         }
         if (L.seq) {
-            *c = make_uint2(val.x, val.y);
+            sts2(ca, val.x, val.y);
             return true;
         }
-        L.wbits[(w >> 5) * L.bit_row] |= bit;
+        {
+            const uint32_t ba = L.wsh + (w >> 5) * L.bstr;
+            sts1(ba, lds1(ba) | bit);
+        }
         // Same-phase stores of several simulated threads: the highest thread id
         // wins, and a thread's own stores land in program order (the
         // reference runs threads one after another, src/vm.cpp:121-142).
         const uint32_t me = static_cast<uint32_t>(L.tid) + 1;
         const uint32_t meta = val.y | (me << 8) | (L.epoch << 16);
-        unsigned long long* cp = reinterpret_cast<unsigned long long*>(c);
-        const unsigned long long want =
-            (static_cast<unsigned long long>(meta) << 32) | val.x;
-        unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(cp);
+        const unsigned long long want = (static_cast<unsigned long long>(meta) << 32) | val.x;
+        unsigned long long cur = lds64(ca);
         for (;;) {
             const uint32_t m = static_cast<uint32_t>(cur >> 32);
             if ((m >> 16) == L.epoch && ((m >> 8) & 0xFF) > me)
                 break;
-            const unsigned long long prev = atomicCAS(cp, cur, want);
+            const unsigned long long prev = cas64(ca, cur, want);
             if (prev == cur)
                 break;
             cur = prev;
@@ -925,11 +964,10 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
         return true;
     }
     const uint32_t prm = p.y & 0x3F;
-    const size_t tp = static_cast<size_t>(L.t) * A.n_params + prm;
-    const int32_t size = __ldg(A.buf_size + tp);
-    if (eff < 0 || eff >= size)
+    const uint32_t info = __ldg(L.binfo + prm);
+    if (eff < 0 || eff >= static_cast<int32_t>(info >> 8))
         return L.trap(GEVO_TRAP_GLOBAL_OOB);
-    const uint32_t elem = __ldg(A.buf_elem + tp);
+    const uint32_t elem = info & 0xFF;
     const bool priv = (L.writable >> prm) & 1ull;
     if (op == GEVO_OP_LOAD) {
         if (elem != f_aux(r))
@@ -989,7 +1027,7 @@ __device__ __forceinline__ bool misc_op(const InterpArgs& A, Lane<kM>& L, const 
 // run_to_barrier (vm.cpp:340-387) + step (389-482) for one simulated thread
 // from (th.block, th.ip). Returns kStopRet, kStopSync or kStopTrap.
 template <int kM>
-__device__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th, const int64_t* s_cost,
+__device__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th,
                           const volatile int32_t* first_fail) {
     Spin S;
     S.mode = 0;
@@ -998,38 +1036,34 @@ __device__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th, const in
     S.next = A.sp_base ? A.spin_threshold : INT64_MAX;
     int64_t bcost;
     Blk b = load_blk(L.dblk, th.block, bcost);
-    charge_block(A, L, th, b, bcost, static_cast<uint32_t>(th.ip), s_cost);
-    uint4 nxt = fetch_inst(L.code, b.start + static_cast<uint32_t>(th.ip));
+    charge_block(A, L, th, b, bcost, static_cast<uint32_t>(th.ip));
+    const uint4* code = reinterpret_cast<const uint4*>(L.code);
+    // pc indexes the variant's records; every block is followed by a
+    // fell-off sentinel record, and the batch array is padded, so the
+    // one-ahead prefetch never leaves it.
+    uint32_t pc = b.start + static_cast<uint32_t>(th.ip);
+    uint4 nxt = __ldg(code + pc);
     for (;;) {
-        const uint32_t ip = static_cast<uint32_t>(th.ip);
-        if (ip >= b.len) {
-            L.trap(GEVO_TRAP_FELL_OFF);
-            return kStopTrap;
-        }
         const uint4 r = nxt;
-        // prefetch the next record of the block (the batch array is padded)
-        nxt = fetch_inst(L.code, b.start + ip + 1);
+        nxt = __ldg(code + pc + 1);
         const uint32_t op = f_op(r);
-        if (op == GEVO_OP_PHI) {
-            refund(L, th, b, ip, s_cost);
-            L.trap(GEVO_TRAP_PHI_OUTSIDE);
-            return kStopTrap;
+        if (th.slow || S.mode == 2) {
+            // exact per-instruction charging near the budget / abstract iterate
+            if (op != GEVO_OP_PHI && op != GEVO_OP_FELL) {
+                if (th.slow && !charge_one(A, L, th, f_cls(r))) {
+                    th.ip = static_cast<int32_t>(pc - b.start);
+                    return kStopTrap;
+                }
+                if (S.mode == 2 && !spin_track(A, L, r, S))
+                    spin_abandon(S, th, L, 0x80 | op);
+            }
         }
-        if (th.slow && !charge_one(A, L, th, f_cls(r), s_cost))
-            return kStopTrap;
-        if (S.mode == 2 && !spin_track(A, L, r, S))
-            spin_abandon(S, th, L, 0x80 | op);
-
         bool ok;
         if (op <= GEVO_OP_FCMP) {
             // i32 / f32 arithmetic and compares: both operands carry otag
             const uint2 x = L.V(f_a(r)), y = L.V(f_b(r));
             const uint32_t otag = f_otag(r);
-            if (x.y != otag) {
-                ok = L.scalar_fail(f_a(r), x.y);
-            } else if (y.y != otag) {
-                ok = L.scalar_fail(f_b(r), y.y);
-            } else {
+            if (x.y == otag && y.y == otag) {
                 uint32_t v;
                 uint32_t vt = otag;
                 ok = true;
@@ -1060,21 +1094,33 @@ __device__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th, const in
                     vt = GEVO_TAG_BOOL;
                     break;
                 }
+                const uint32_t res = f_res(r);
+                if (ok && res != GEVO_NO_RESULT) {
+                    L.W(res, v, vt);
+                    ++pc;
+                    continue;
+                }
                 if (ok)
-                    ok = L.set(f_res(r), v, vt);
+                    L.trap(GEVO_TRAP_DEF_NO_ID);
+            } else if (x.y != otag) {
+                L.scalar_fail(f_a(r), x.y);
+            } else {
+                L.scalar_fail(f_b(r), y.y);
             }
+            ok = false;
         } else if (op == GEVO_OP_BR) {
+            th.ip = static_cast<int32_t>(pc - b.start);
             int32_t target = f_t0(r);
             if (f_aux(r) == 2) {
                 const uint2 c = L.V(f_a(r));
                 if (c.y != GEVO_TAG_BOOL) {
                     L.scalar_fail(f_a(r), c.y);
-                    refund(L, th, b, ip + 1, s_cost);
+                    refund(A, L, th, b, th.ip + 1);
                     return kStopTrap;
                 }
                 target = c.x ? f_t0(r) : f_t1(r);
             }
-            refund(L, th, b, ip + 1, s_cost);
+            refund(A, L, th, b, th.ip + 1);
             if (target < 0) {
                 L.trap(GEVO_TRAP_UNKNOWN_BLOCK);
                 return kStopTrap;
@@ -1083,7 +1129,7 @@ __device__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th, const in
                 // a lower simulated thread already stopped the instance
                 if (--L.poll <= 0) {
                     L.poll = 16;
-                    if (*L.min_stop < L.tid)
+                    if (static_cast<int32_t>(lds1(L.msh)) < L.tid)
                         return kStopAbort;
                     if (A.early_exit && (++L.poll2 & 127) == 0 &&
                         first_fail[L.v] < static_cast<int32_t>(L.t)) {
@@ -1098,29 +1144,38 @@ __device__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th, const in
                     return kStopTrap;
                 }
             }
-            if (!enter_block(A, L, th, s_cost, target, b, S))
+            if (!enter_block(A, L, th, target, b, S))
                 return kStopTrap;
             if ((th.executed >= S.next || S.mode != 0) && !th.slow)
                 spin_at_entry(A, L, th, S);
-            nxt = fetch_inst(L.code, b.start + static_cast<uint32_t>(th.ip));
+            pc = b.start + static_cast<uint32_t>(th.ip);
+            nxt = __ldg(code + pc);
             continue;
         } else if (op == GEVO_OP_LOAD || op == GEVO_OP_STORE) {
             ok = mem_op(A, L, r);
-        } else if (op == GEVO_OP_SYNC) {
-            refund(L, th, b, ip + 1, s_cost);
+        } else if (op == GEVO_OP_SYNC || op == GEVO_OP_RET) {
+            th.ip = static_cast<int32_t>(pc - b.start);
+            refund(A, L, th, b, th.ip + 1);
             th.bar = f_b(r);
-            return kStopSync;
-        } else if (op == GEVO_OP_RET) {
-            refund(L, th, b, ip + 1, s_cost);
-            return kStopRet;
+            return op == GEVO_OP_SYNC ? kStopSync : kStopRet;
+        } else if (op == GEVO_OP_PHI) {
+            th.ip = static_cast<int32_t>(pc - b.start);
+            refund(A, L, th, b, th.ip);
+            L.trap(GEVO_TRAP_PHI_OUTSIDE);
+            return kStopTrap;
+        } else if (op == GEVO_OP_FELL) {
+            th.ip = static_cast<int32_t>(pc - b.start);
+            L.trap(GEVO_TRAP_FELL_OFF);
+            return kStopTrap;
         } else {
             ok = misc_op(A, L, r);
         }
         if (!ok) {
-            refund(L, th, b, ip + 1, s_cost);
+            th.ip = static_cast<int32_t>(pc - b.start);
+            refund(A, L, th, b, th.ip + 1);
             return kStopTrap;
         }
-        ++th.ip;
+        ++pc;
     }
 }
 
@@ -1139,7 +1194,7 @@ __device__ __forceinline__ void reset_values(Lane<kM>& L) {
 // Machine::run for one instance (src/vm.cpp:114-150). Returns the status.
 template <int kM>
 __device__ uint32_t run_instance(const InterpArgs& A, Lane<kM>& L, const gevo_variant& var,
-                                 const int64_t* s_cost, const volatile int32_t* first_fail) {
+                                 const volatile int32_t* first_fail) {
     const int32_t T = A.threads;
     if (!(var.flags & GEVO_VAR_HAS_SYNC)) {
         // No barrier instruction: every thread runs to ret in phase 0.
@@ -1147,7 +1202,7 @@ __device__ uint32_t run_instance(const InterpArgs& A, Lane<kM>& L, const gevo_va
             reset_values(L);
             L.tid = tid;
             Thread th{0, 0, -1, 0, 0, false};
-            const int r = run_thread(A, L, th, s_cost, first_fail);
+            const int r = run_thread(A, L, th, first_fail);
             if (r == kStopTrap)
                 return status_of(L.code_out);
             if (r != kStopRet) {
@@ -1192,7 +1247,7 @@ __device__ uint32_t run_instance(const InterpArgs& A, Lane<kM>& L, const gevo_va
                     }
                 }
                 L.tid = tid;
-                const int r = run_thread(A, L, th, s_cost, first_fail);
+                const int r = run_thread(A, L, th, first_fail);
                 if (r == kStopTrap)
                     return status_of(L.code_out);
                 A.ts_pos[at] = (th.block << 16) | th.ip;
@@ -1262,11 +1317,6 @@ __device__ double instance_error(const InterpArgs& A, const Lane<kM>& L) {
 
 template <int kM>
 __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ InterpArgs A) {
-    __shared__ int64_t s_cost[GEVO_COST_CLASSES];
-    if (threadIdx.x < GEVO_COST_CLASSES)
-        s_cost[threadIdx.x] = A.cost[threadIdx.x];
-    __syncthreads();
-
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp;
     const uint32_t vl = gw / A.warps_per_variant; // variant, local to the launch
@@ -1284,10 +1334,13 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
     L.il = il;
     L.sl = il;
     L.seq = true;
+    L.binfo = A.buf_info + static_cast<size_t>(t) * A.n_params;
     if (Lane<kM>::kSmem) {
         L.gvf = nullptr;
         L.base = warp * A.row_lanes * A.max_slots + (lane & (A.row_lanes - 1));
         L.row = A.row_lanes;
+        L.vsh = smem_addr(g_vfs) + L.base * 8;
+        L.vstr = A.row_lanes * 8;
     } else {
         L.gvf = A.vf;
         L.base = il;
@@ -1349,7 +1402,7 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
         for (int32_t w = 0; w < A.shared_words; ++w)
             A.sh_tag[static_cast<size_t>(w) * A.n_inst + il] = GEVO_TAG_UNDEF;
 
-        status = run_instance(A, L, var, s_cost, first_fail);
+        status = run_instance(A, L, var, first_fail);
         if (status == GEVO_STATUS_COMPLETED)
             error = instance_error(A, L);
     }
@@ -1370,148 +1423,130 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
         atomicMin(A.first_fail + v, static_cast<int32_t>(t));
 }
 
-// ---- thread-parallel lanes ---------------------------------------------------
+// ---- thread-parallel interpreter ---------------------------------------------
 //
-// interp_tp_kernel gives every simulated thread of an instance its own lane:
-// a group of G lanes (G = threads rounded up to a power of two, <= 32) runs
-// one (variant, test) instance, 32 / G instances per warp, consecutive tests of
-// one variant side by side. A phase (the stretch between two barriers) runs
-// all threads at once instead of one after another; the instance's mutable
-// memory -- simulated shared words and its private copies of writable global
-// buffers -- lives in shared-memory cells {payload, tag | writer << 8 |
-// epoch << 16}.
+// interp_tp_kernel runs the simulated threads of an instance concurrently on
+// different warps: a CTA holds one variant and up to 32 consecutive tests;
+// warp u runs simulated thread u of every test, lane j test tg * 32 + j. The
+// lanes of a warp execute the same variant and the same thread id on
+// different inputs, so they stay converged like the sequential-lane kernel,
+// while the threads of one instance no longer queue behind each other. The
+// instance's mutable memory -- simulated shared words and its private copies
+// of writable global buffers -- lives in shared-memory cells {payload, tag |
+// writer << 8 | epoch << 16}, one column per test.
 //
-// Exactness. Within a phase the reference runs threads in id order
-// (src/vm.cpp:121-142), so thread t sees every write of threads < t and none
-// of threads > t. Running them concurrently gives the same result whenever no
-// word is read by one thread and written by another in the same phase: every
-// read then returns the phase-start value or the reader's own write. Words
-// only written by several threads (nw-sync's s[80]) keep the value of the
-// highest writer -- each store is a compare-and-swap that never overwrites a
-// higher writer of the current epoch, and a thread's own stores land in
-// program order. Every lane records the words it read and wrote in per-phase
-// bitsets; at the phase end the group checks R_t & (W of any other thread);
-// any hit discards the parallel run and re-executes the whole instance with
-// threads in id order (plain stores), i.e. the reference schedule.
+// Exactness. Within a phase (the stretch between two barriers) the reference
+// runs threads in id order (src/vm.cpp:121-142), so thread t sees every write
+// of threads < t and none of threads > t. Running them concurrently gives the
+// same result whenever no word is read by one thread and written by another in
+// the same phase: every read then returns the phase-start value or the
+// reader's own write. Words only written by several threads (nw-sync's s[80])
+// keep the value of the highest writer -- each store is a compare-and-swap
+// that never overwrites a higher writer of the current epoch, and a thread's
+// own stores land in program order. Every thread records the words it read and
+// wrote in per-phase bitsets; at the phase end R_t & (W of any other thread)
+// is checked, and any hit discards the concurrent run of that instance and
+// re-executes it from the start with its threads in id order (the reference
+// schedule, plain stores).
 //
 // Stops. The lowest thread id that traps (or exceeds its budget) decides the
 // record, as in the reference, where higher threads never run after it: the
 // cost and dynamic IR of threads above it in that phase are dropped, and those
-// lanes abandon their run early (min_stop poll). Barrier divergence is judged
-// on all threads once none trapped (vm.cpp:123-137).
+// threads abandon their run early (min_stop poll). Barrier divergence is
+// judged on all threads once none trapped (vm.cpp:123-137).
 
 namespace {
 
-struct TpLayout {
-    uint32_t vf_words;     // uint2 entries of value files per CTA
-    uint32_t cell_words;   // uint2 cells per CTA
-    uint32_t bit_words;    // uint32 per bitset (R or W) per CTA
+constexpr uint32_t kTpMaxThreads = 8; // warps per CTA
+enum : uint32_t { kInstPar = 0, kInstSeq = 1, kInstDone = 2 };
+enum : uint32_t { kActContinue = 0, kActFinish = 1, kActRestart = 2 };
+
+struct TpShared {
+    int32_t min_stop[32];
+    uint32_t state[32];
+    uint32_t conflict[32];
+    uint32_t status[32];
+    uint32_t code[32];
+    int32_t aux[32];
+    unsigned long long cost[32];
+    unsigned long long ir[32];
+    uint32_t jumps[32];
+    uint32_t kind[kTpMaxThreads][32];
+    uint32_t bar[kTpMaxThreads][32];
+    uint32_t tcode[kTpMaxThreads][32];
+    int32_t taux[kTpMaxThreads][32];
+    double err[kTpMaxThreads][32];
 };
 
-__device__ __forceinline__ TpLayout tp_layout(const InterpArgs& A, uint32_t warps) {
-    TpLayout l;
-    l.vf_words = warps * 32 * A.max_slots;
-    l.cell_words = warps * (32 / A.tp_group) * A.n_cells;
-    l.bit_words = warps * 32 * A.n_chunks;
-    return l;
-}
-
-template <typename T>
-__device__ __forceinline__ T group_sum(T x, uint32_t gmask, uint32_t G) {
-    for (uint32_t o = 1; o < G; o <<= 1)
-        x += __shfl_xor_sync(gmask, x, o, G);
-    return x;
-}
-
-// Conflict of the phase: some thread read a word another thread wrote.
-__device__ __forceinline__ bool group_conflict(const Lane<2>& L, uint32_t nch, uint32_t gmask,
-                                               uint32_t G) {
-    uint32_t hit = 0;
-    for (uint32_t k = 0; k < nch; ++k) {
-        const uint32_t w = L.wbits[k * L.bit_row], r = L.rbits[k * L.bit_row];
-        uint32_t a1 = w, a2 = 0; // written by >= 1 / >= 2 threads
-        for (uint32_t o = 1; o < G; o <<= 1) {
-            const uint32_t b1 = __shfl_xor_sync(gmask, a1, o, G);
-            const uint32_t b2 = __shfl_xor_sync(gmask, a2, o, G);
-            a2 |= b2 | (a1 & b1);
-            a1 |= b1;
-        }
-        hit |= r & (a2 | (a1 & ~w));
-    }
-    return __any_sync(gmask, hit != 0);
-}
-
-// (Re)initialises the instance: memory cells from the test's inputs, the
-// lane's value file, counters.
-__device__ __forceinline__ void tp_init_instance(const InterpArgs& A, Lane<2>& L, uint32_t tid,
-                                                 uint32_t G, uint32_t gmask) {
+// Instance memory cells from the test's inputs; warp u fills words u, u+T, ...
+__device__ __forceinline__ void tp_init_cells(const InterpArgs& A, const Lane<2>& L, uint32_t u,
+                                              uint32_t T) {
     const uint32_t SW = static_cast<uint32_t>(max(A.shared_words, 0));
-    for (uint32_t w = tid; w < SW; w += G)
-        *L.cell(w) = make_uint2(0, GEVO_TAG_UNDEF);
+    for (uint32_t w = u; w < SW; w += T)
+        sts2(L.cell(w), 0, GEVO_TAG_UNDEF);
     const size_t tp0 = static_cast<size_t>(L.t) * A.n_params;
     for (uint64_t m = L.writable; m; m &= m - 1) {
         const uint32_t p = static_cast<uint32_t>(__ffsll(static_cast<long long>(m)) - 1);
         const int32_t rows = A.buf_size[tp0 + p];
         const uint32_t elem = A.buf_elem[tp0 + p];
-        for (int32_t e = static_cast<int32_t>(tid); e < rows; e += static_cast<int32_t>(G))
-            *L.cell(A.cell_off[p] + static_cast<uint32_t>(e)) = make_uint2(
-                __ldg(A.pool + A.pool_off[p] + static_cast<size_t>(e) * A.n_tests + L.t), elem);
+        for (int32_t e = static_cast<int32_t>(u); e < rows; e += static_cast<int32_t>(T))
+            sts2(L.cell(A.cell_off[p] + static_cast<uint32_t>(e)),
+                 __ldg(A.pool + A.pool_off[p] + static_cast<size_t>(e) * A.n_tests + L.t), elem);
     }
+}
+
+__device__ __forceinline__ void tp_reset_thread(Lane<2>& L, Thread& th) {
     for (uint32_t s = 0; s < L.n_values; ++s)
         L.W(s, 0, GEVO_TAG_UNDEF);
     L.cost = 0;
     L.ir = 0;
     L.code_out = GEVO_OK;
     L.aux = 0;
-    __syncwarp(gmask);
+    th = Thread{0, 0, -1, 0, 0, false};
 }
 
 } // namespace
 
-__global__ void __launch_bounds__(128) interp_tp_kernel(const __grid_constant__ InterpArgs A) {
-    __shared__ int64_t s_cost[GEVO_COST_CLASSES];
-    if (threadIdx.x < GEVO_COST_CLASSES)
-        s_cost[threadIdx.x] = A.cost[threadIdx.x];
-    __syncthreads();
+__global__ void __launch_bounds__(256, 2) interp_tp_kernel(const __grid_constant__ InterpArgs A) {
+    __shared__ TpShared S;
+    const uint32_t T = blockDim.x >> 5;            // simulated threads = warps
+    const uint32_t u = threadIdx.x >> 5, j = threadIdx.x & 31;
 
-    const uint32_t warps = blockDim.x >> 5;
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t G = A.tp_group, gpw = 32 / G;
-    const uint32_t tid = lane & (G - 1);
-    const uint32_t gbase = lane & ~(G - 1);
-    const uint32_t gmask = G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1) << gbase);
-    const uint32_t ic = warp * gpw + lane / G;            // instance within the CTA
-    const uint32_t inst = blockIdx.x * warps * gpw + ic;  // instance within the launch
-    if (inst >= A.n_inst)
-        return; // whole group
     const uint32_t nt = static_cast<uint32_t>(A.n_tests);
-    const uint32_t vl = inst / nt, t = inst % nt;
+    const uint32_t tgroups = (nt + A.tp_lanes - 1) / A.tp_lanes;
+    const uint32_t vl = blockIdx.x / tgroups;
+    const uint32_t t = (blockIdx.x % tgroups) * A.tp_lanes + j;
     const uint32_t v = A.v_begin + vl;
+    const bool valid = j < A.tp_lanes && t < nt;
     const uint64_t gi = static_cast<uint64_t>(v) * nt + t;
-    const bool active = tid < static_cast<uint32_t>(A.threads);
-    const uint32_t amask = __ballot_sync(gmask, active) >> gbase; // group-relative
 
-    const TpLayout lay = tp_layout(A, warps);
-    uint32_t* bits = reinterpret_cast<uint32_t*>(g_vfs + lay.vf_words + lay.cell_words);
-    int32_t* s_min_stop = reinterpret_cast<int32_t*>(bits + 2 * lay.bit_words);
+    const uint32_t Ln = A.tp_lanes;                // tests (lanes) per CTA
+    const uint32_t sbase = smem_addr(g_vfs);
+    const uint32_t cell0 = sbase + T * Ln * A.max_slots * 8;
+    const uint32_t bits0 = cell0 + Ln * A.n_cells * 8;
+    const uint32_t bit_words = A.n_chunks * blockDim.x;
+    uint32_t* bits = reinterpret_cast<uint32_t*>(g_vfs + (T * Ln * A.max_slots + Ln * A.n_cells));
 
     Lane<2> L;
     L.gvf = nullptr;
-    L.base = warp * 32 * A.max_slots + lane;
-    L.row = 32;
+    L.vsh = sbase + (u * Ln * A.max_slots + j) * 8;
+    L.vstr = Ln * 8;
+    L.base = 0;
+    L.row = 0;
     L.v = v;
-    L.t = t;
-    L.il = inst;
-    L.sl = inst * G + tid;
-    L.tid = static_cast<int32_t>(tid);
-    L.cells = g_vfs + lay.vf_words + ic;
-    L.cell_row = warps * gpw;
-    L.rbits = bits + threadIdx.x;
-    L.wbits = bits + lay.bit_words + threadIdx.x;
-    L.bit_row = blockDim.x;
+    L.t = valid ? t : 0;
+    L.il = blockIdx.x * 32 + j;
+    L.sl = blockIdx.x * blockDim.x + threadIdx.x;
+    L.tid = static_cast<int32_t>(u);
+    L.binfo = A.buf_info + static_cast<size_t>(L.t) * A.n_params;
+    L.csh = cell0 + j * 8;
+    L.cstr = Ln * 8;
+    L.rsh = bits0 + threadIdx.x * 4;
+    L.wsh = L.rsh + bit_words * 4;
+    L.bstr = blockDim.x * 4;
+    L.msh = smem_addr(S.min_stop + j);
     L.epoch = 0;
     L.seq = false;
-    L.min_stop = s_min_stop + ic;
     L.cost = 0;
     L.ir = 0;
     L.poll = 16;
@@ -1521,22 +1556,40 @@ __global__ void __launch_bounds__(128) interp_tp_kernel(const __grid_constant__ 
     L.code_out = GEVO_OK;
     L.aux = 0;
     L.writable = 0;
+    L.n_values = 0;
 
     const volatile int32_t* first_fail = A.first_fail;
-    uint32_t status = GEVO_STATUS_TRAP;
-    double error = -1.0;
-    int64_t cost_total = 0, ir_total = 0;
-    const uint8_t setup = A.setup_code[t];
-    if (A.early_exit && first_fail[v] < static_cast<int32_t>(t)) {
-        L.code_out = GEVO_SKIPPED;
-        status = GEVO_STATUS_SKIPPED;
-    } else if (setup != GEVO_OK) {
-        L.code_out = setup;
-        L.aux = A.setup_aux[t];
-        status = GEVO_STATUS_TRAP;
-    } else {
-        const gevo_variant var = A.variants[v];
-        const uint32_t P = static_cast<uint32_t>(A.n_params);
+    const uint8_t setup = valid ? A.setup_code[t] : GEVO_OK;
+    if (u == 0) {
+        S.cost[j] = 0;
+        S.ir[j] = 0;
+        S.jumps[j] = 0;
+        S.aux[j] = 0;
+        if (!valid) {
+            S.state[j] = kInstDone;
+            S.status[j] = GEVO_STATUS_SKIPPED;
+            S.code[j] = GEVO_SKIPPED;
+        } else if (A.early_exit && first_fail[v] < static_cast<int32_t>(t)) {
+            S.state[j] = kInstDone;
+            S.status[j] = GEVO_STATUS_SKIPPED;
+            S.code[j] = GEVO_SKIPPED;
+        } else if (setup != GEVO_OK) {
+            // Machine ctor failure: trap with cost 0 (src/vm.cpp:516-520).
+            S.state[j] = kInstDone;
+            S.status[j] = GEVO_STATUS_TRAP;
+            S.code[j] = setup;
+            S.aux[j] = A.setup_aux[t];
+        } else {
+            S.state[j] = kInstPar;
+        }
+    }
+    __syncthreads();
+
+    const gevo_variant var = A.variants[v];
+    const uint32_t P = static_cast<uint32_t>(A.n_params);
+    Thread th{0, 0, -1, 0, 0, false};
+    int64_t cost_commit = 0, ir_commit = 0;
+    if (S.state[j] != kInstDone) {
         L.code = A.insts + var.inst_base;
         L.dblk = A.dblocks + var.block_base;
         L.arm = A.arms + var.arm_base;
@@ -1553,126 +1606,179 @@ __global__ void __launch_bounds__(128) interp_tp_kernel(const __grid_constant__ 
         for (uint32_t k = 0; k < var.n_lits; ++k)
             L.W(lit_begin + k, __ldg(A.lit_payload + var.lit_base + k),
                 __ldg(A.lit_tag + var.lit_base + k));
-        tp_init_instance(A, L, tid, G, gmask);
+        tp_reset_thread(L, th);
+        tp_init_cells(A, L, u, T);
+    }
 
-        Thread th{0, 0, -1, 0, 0, false};
-        int64_t cost_commit = 0, ir_commit = 0;
-        for (;;) { // phases
-            ++L.epoch;
-            if (!L.seq) {
-                for (uint32_t k = 0; k < A.n_chunks; ++k) {
-                    L.rbits[k * L.bit_row] = 0;
-                    L.wbits[k * L.bit_row] = 0;
-                }
+    for (;;) { // phases, CTA-uniform
+        ++L.epoch;
+        const uint32_t st = S.state[j];
+        if (st == kInstPar) {
+            for (uint32_t k = 0; k < A.n_chunks; ++k) {
+                sts1(L.rsh + k * L.bstr, 0);
+                sts1(L.wsh + k * L.bstr, 0);
             }
-            if (tid == 0)
-                *const_cast<int32_t*>(L.min_stop) = INT32_MAX;
-            __syncwarp(gmask);
-            int kind = kStopIdle;
-            bool restart = false;
-            if (!L.seq) {
-                if (active) {
-                    kind = run_thread(A, L, th, s_cost, first_fail);
+        }
+        if (u == 0) {
+            S.min_stop[j] = INT32_MAX;
+            S.conflict[j] = 0;
+        }
+        __syncthreads();
+        int kind = kStopIdle;
+        if (st == kInstPar) {
+            L.seq = false;
+            kind = run_thread(A, L, th, first_fail);
+            if (kind == kStopTrap)
+                atomicMin(S.min_stop + j, static_cast<int32_t>(u));
+        }
+        if (__syncthreads_or(st == kInstSeq)) {
+            // reference schedule: thread after thread, stop at the first trap
+            for (uint32_t w = 0; w < T; ++w) {
+                if (w == u && st == kInstSeq && S.min_stop[j] == INT32_MAX) {
+                    L.seq = true;
+                    kind = run_thread(A, L, th, first_fail);
                     if (kind == kStopTrap)
-                        atomicMin(const_cast<int32_t*>(L.min_stop), L.tid);
+                        S.min_stop[j] = static_cast<int32_t>(u);
                 }
-                __syncwarp(gmask);
-                restart = L.epoch >= 0xFFFFu || group_conflict(L, A.n_chunks, gmask, G);
+                __syncthreads();
+            }
+        }
+        S.kind[u][j] = static_cast<uint32_t>(kind);
+        S.bar[u][j] = th.bar;
+        S.tcode[u][j] = L.code_out;
+        S.taux[u][j] = L.aux;
+        __syncthreads();
+        if (st == kInstPar) {
+            // same-phase cross-thread read/write: R_u & W_w, w != u
+            uint32_t hit = 0;
+            for (uint32_t k = 0; k < A.n_chunks && !hit; ++k) {
+                const uint32_t r = lds1(L.rsh + k * L.bstr);
+                if (!r)
+                    continue;
+                for (uint32_t w = 0; w < T; ++w)
+                    if (w != u)
+                        hit |= r & bits[bit_words + k * blockDim.x + w * 32 + j];
+            }
+            if (hit)
+                S.conflict[j] = 1;
+        }
+        __syncthreads();
+        // Phase verdict of instance j (every warp derives the same one).
+        uint32_t act = kActContinue, ts = T, status = 0;
+        if (st == kInstDone) {
+            act = kActFinish + 8; // nothing to do
+        } else if (S.conflict[j] || (st == kInstPar && L.epoch >= 0xFFFFu)) {
+            act = kActRestart;
+        } else {
+            for (uint32_t w = 0; w < T; ++w)
+                if (S.kind[w][j] == kStopTrap) {
+                    ts = w;
+                    break;
+                }
+            if (ts < T) {
+                act = kActFinish;
+                const uint32_t c = S.tcode[ts][j];
+                status = c == GEVO_BUDGET_EXCEEDED ? GEVO_STATUS_BUDGET
+                         : c == GEVO_SKIPPED      ? GEVO_STATUS_SKIPPED
+                                                  : GEVO_STATUS_TRAP;
             } else {
-                for (uint32_t u = 0; u < static_cast<uint32_t>(A.threads); ++u) {
-                    if (tid == u)
-                        kind = run_thread(A, L, th, s_cost, first_fail);
-                    if (__shfl_sync(gmask, kind, u, G) == kStopTrap)
-                        break;
+                bool all_ret = true, same = true;
+                const uint32_t b0 = S.bar[0][j];
+                for (uint32_t w = 0; w < T; ++w) {
+                    const uint32_t k = S.kind[w][j];
+                    all_ret &= k == kStopRet;
+                    same &= k == kStopSync && S.bar[w][j] == b0;
+                }
+                if (all_ret) {
+                    act = kActFinish;
+                    status = GEVO_STATUS_COMPLETED;
+                } else if (!same) {
+                    act = kActFinish;
+                    status = GEVO_STATUS_TRAP;
+                    ts = T + 1; // divergence
                 }
             }
-            if (restart) {
-                // reference schedule from the start: threads in id order
-                if (A.counters && tid == 0)
-                    atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 2), 1ull);
-                L.seq = true;
-                L.epoch = 0;
-                th = Thread{0, 0, -1, 0, 0, false};
-                cost_commit = ir_commit = 0;
-                __syncwarp(gmask);
-                tp_init_instance(A, L, tid, G, gmask);
-                continue;
+        }
+        __syncthreads(); // verdict inputs read; shared state may change now
+        if (act == kActRestart) {
+            if (A.counters && u == 0)
+                atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 2), 1ull);
+            tp_reset_thread(L, th);
+            tp_init_cells(A, L, u, T);
+            cost_commit = ir_commit = 0;
+            if (u == 0)
+                S.state[j] = kInstSeq;
+        } else if (act == kActFinish) {
+            const bool mine = ts >= T || u <= ts;
+            atomicAdd(S.cost + j, static_cast<unsigned long long>(mine ? L.cost : cost_commit));
+            atomicAdd(S.ir + j, static_cast<unsigned long long>(mine ? L.ir : ir_commit));
+            atomicAdd(S.jumps + j, L.jumps);
+            if (u == 0) {
+                S.state[j] = kInstDone;
+                S.status[j] = status;
+                if (ts < T) {
+                    S.code[j] = S.tcode[ts][j];
+                    S.aux[j] = S.taux[ts][j];
+                } else if (ts == T + 1) {
+                    S.code[j] = GEVO_TRAP_DIVERGENCE;
+                    S.aux[j] = 0;
+                } else {
+                    S.code[j] = GEVO_OK;
+                    S.aux[j] = 0;
+                }
             }
-            const uint32_t traps = (__ballot_sync(gmask, kind == kStopTrap) >> gbase) & amask;
-            if (traps) {
-                const uint32_t ts = __ffs(traps) - 1;
-                const bool mine = tid <= ts;
-                cost_total = group_sum<long long>(mine ? L.cost : cost_commit, gmask, G);
-                ir_total = group_sum<long long>(mine ? L.ir : ir_commit, gmask, G);
-                L.code_out = __shfl_sync(gmask, L.code_out, ts, G);
-                L.aux = __shfl_sync(gmask, L.aux, ts, G);
-                status = L.code_out == GEVO_BUDGET_EXCEEDED ? GEVO_STATUS_BUDGET
-                         : L.code_out == GEVO_SKIPPED      ? GEVO_STATUS_SKIPPED
-                                                           : GEVO_STATUS_TRAP;
-                break;
-            }
-            cost_total = group_sum<long long>(L.cost, gmask, G);
-            ir_total = group_sum<long long>(L.ir, gmask, G);
-            const uint32_t rets = (__ballot_sync(gmask, kind == kStopRet) >> gbase) & amask;
-            if (rets == amask) {
-                status = GEVO_STATUS_COMPLETED;
-                break;
-            }
-            const uint32_t bar0 = __shfl_sync(gmask, th.bar, 0, G);
-            const uint32_t same =
-                (__ballot_sync(gmask, kind == kStopSync && th.bar == bar0) >> gbase) & amask;
-            if (same != amask) {
-                L.code_out = GEVO_TRAP_DIVERGENCE;
-                L.aux = 0;
-                status = GEVO_STATUS_TRAP;
-                break;
-            }
+        } else if (act == kActContinue) {
             ++th.ip; // step past the barrier
             cost_commit = L.cost;
             ir_commit = L.ir;
         }
-        if (status == GEVO_STATUS_COMPLETED) {
-            // compute_error (src/vm.cpp:536-556): max over oracle elements,
-            // spread over the group's lanes (max is order-free).
-            double worst = 0.0;
-            if (A.static_err[t]) {
-                worst = 1.0;
-            } else {
-                for (int32_t e = A.entry_begin[t]; e < A.entry_begin[t + 1]; ++e) {
-                    const OracleEntryDev en = A.entries[e];
-                    const uint32_t p = static_cast<uint32_t>(en.param);
-                    const bool priv = (L.writable >> p) & 1ull;
-                    for (int32_t k = static_cast<int32_t>(tid); k < en.size;
-                         k += static_cast<int32_t>(G)) {
-                        const uint32_t cw =
-                            priv ? L.cell(A.cell_off[p] + static_cast<uint32_t>(k))->x
-                                 : __ldg(A.pool + A.pool_off[p] + static_cast<size_t>(k) * nt + t);
-                        const uint32_t ow = __ldg(A.pool + en.off + static_cast<size_t>(k) * nt + t);
-                        const double d =
-                            rel_diff(word_to_double(cw, en.elem), word_to_double(ow, en.elem));
-                        worst = (worst < d) ? d : worst;
-                    }
-                }
-                for (uint32_t o = 1; o < G; o <<= 1) {
-                    const double x = __shfl_xor_sync(gmask, worst, o, G);
-                    worst = (worst < x) ? x : worst;
-                }
+        if (__syncthreads_and(S.state[j] == kInstDone))
+            break;
+    }
+
+    // compute_error (src/vm.cpp:536-556) of completed instances: max over
+    // oracle elements, spread over the warps (max is order-free).
+    double worst = 0.0;
+    const bool done_ok = S.status[j] == GEVO_STATUS_COMPLETED;
+    if (done_ok && !A.static_err[t]) {
+        for (int32_t e = A.entry_begin[t]; e < A.entry_begin[t + 1]; ++e) {
+            const OracleEntryDev en = A.entries[e];
+            const uint32_t p = static_cast<uint32_t>(en.param);
+            const bool priv = (L.writable >> p) & 1ull;
+            for (int32_t k = static_cast<int32_t>(u); k < en.size; k += static_cast<int32_t>(T)) {
+                const uint32_t cw = priv ? lds2(L.cell(A.cell_off[p] + static_cast<uint32_t>(k))).x
+                                         : __ldg(A.pool + A.pool_off[p] +
+                                                 static_cast<size_t>(k) * nt + t);
+                const uint32_t ow = __ldg(A.pool + en.off + static_cast<size_t>(k) * nt + t);
+                const double d = rel_diff(word_to_double(cw, en.elem), word_to_double(ow, en.elem));
+                worst = (worst < d) ? d : worst;
             }
-            error = worst;
         }
     }
-    const uint32_t jumps = group_sum<uint32_t>(L.jumps, gmask, G);
-    if (tid != 0)
+    S.err[u][j] = worst;
+    __syncthreads();
+    if (u != 0 || !valid)
         return;
+    double error = -1.0;
+    if (done_ok) {
+        if (A.static_err[t]) {
+            error = 1.0;
+        } else {
+            error = 0.0;
+            for (uint32_t w = 0; w < T; ++w)
+                error = (error < S.err[w][j]) ? S.err[w][j] : error;
+        }
+    }
+    const uint32_t status = S.status[j];
     gevo_test_record rec;
-    rec.cost = cost_total;
-    rec.ir = ir_total;
+    rec.cost = static_cast<int64_t>(S.cost[j]);
+    rec.ir = static_cast<int64_t>(S.ir[j]);
     rec.error = error;
-    rec.aux = L.aux;
+    rec.aux = S.aux[j];
     rec.status = static_cast<uint8_t>(status);
-    rec.code = static_cast<uint8_t>(L.code_out);
-    rec.pad[0] = static_cast<uint8_t>(min(jumps, 255u));
-    rec.pad[1] = static_cast<uint8_t>(L.seq ? 1 : 0);
+    rec.code = static_cast<uint8_t>(S.code[j]);
+    rec.pad[0] = static_cast<uint8_t>(min(S.jumps[j], 255u));
+    rec.pad[1] = 0;
     A.rec[gi] = rec;
     if (A.counters)
         atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 3), 1ull);
@@ -1829,17 +1935,24 @@ cudaError_t launch_interp(const InterpArgs& A, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
-TpShape tp_shape(uint32_t group, uint32_t max_slots, uint32_t n_cells, uint32_t n_chunks) {
-    TpShape s{0, 0};
-    for (uint32_t w = 4; w >= 1; w >>= 1) {
-        const size_t inst = static_cast<size_t>(w) * (32 / group);
-        const size_t bytes = static_cast<size_t>(w) * 32 * max_slots * 8 + inst * n_cells * 8 +
-                             2 * static_cast<size_t>(w) * 32 * n_chunks * 4 + inst * 4;
+TpShape tp_shape(uint32_t threads, uint32_t n_tests, uint32_t max_slots, uint32_t n_cells,
+                 uint32_t n_chunks) {
+    TpShape s{0, 0, 0};
+    if (threads < 1 || threads > kTpMaxThreads)
+        return s;
+    // tests per CTA: all of them up to a warp, fewer when the state does not fit
+    for (uint32_t ln = min(max(n_tests, 1u), 32u); ln >= 1; ln = ln > 1 ? (ln + 1) / 2 : 0) {
+        const size_t bytes = static_cast<size_t>(threads) * ln * max_slots * 8 +
+                             static_cast<size_t>(ln) * n_cells * 8 +
+                             2 * static_cast<size_t>(n_chunks) * threads * 32 * 4;
         if (bytes <= kSmemBudget) {
-            s.warps_per_cta = w;
+            s.warps_per_cta = threads;
+            s.lanes = ln;
             s.smem = bytes;
             return s;
         }
+        if (ln == 1)
+            break;
     }
     return s;
 }
@@ -1847,11 +1960,11 @@ TpShape tp_shape(uint32_t group, uint32_t max_slots, uint32_t n_cells, uint32_t 
 cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream) {
     if (A.n_inst == 0)
         return cudaSuccess;
-    const TpShape s = tp_shape(A.tp_group, A.max_slots, A.n_cells, A.n_chunks);
-    if (s.warps_per_cta == 0)
+    const TpShape s = tp_shape(A.tp_group, static_cast<uint32_t>(A.n_tests), A.max_slots,
+                               A.n_cells, A.n_chunks);
+    if (s.warps_per_cta == 0 || s.lanes != A.tp_lanes)
         return cudaErrorInvalidConfiguration;
-    const uint64_t per_cta = static_cast<uint64_t>(s.warps_per_cta) * (32 / A.tp_group);
-    const unsigned grid = static_cast<unsigned>((A.n_inst + per_cta - 1) / per_cta);
+    const unsigned grid = A.n_var * ((static_cast<uint32_t>(A.n_tests) + s.lanes - 1) / s.lanes);
     const cudaError_t e = cudaFuncSetAttribute(
         interp_tp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s.smem));
     if (e != cudaSuccess)

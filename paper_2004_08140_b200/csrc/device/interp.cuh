@@ -35,6 +35,7 @@ struct InterpArgs {
     const uint32_t* param_payload; // [test][param]
     const int32_t* buf_size;       // [test][param]
     const uint8_t* buf_elem;       // [test][param]
+    const uint32_t* buf_info;      // [test][param] size << 8 | elem
     const uint8_t* setup_code;     // [test]
     const int32_t* setup_aux;      // [test]
     const uint32_t* pool;          // inputs + oracles, [row][test] blocks
@@ -88,7 +89,8 @@ struct InterpArgs {
     uint32_t n_spin;                // spin scratch columns (instances, or lanes for tp)
 
     // thread-parallel lanes (interp_tp_kernel)
-    uint32_t tp_group;              // lanes per instance (pow2 >= threads, <= 32)
+    uint32_t tp_group;              // simulated threads = warps per CTA (<= 8)
+    uint32_t tp_lanes;              // tests per CTA (lanes used per warp)
     uint32_t n_cells;               // memory cells per instance: shared words + writable rows
     uint32_t n_chunks;              // 32-bit chunks of a per-lane read / write bitset
     uint32_t cell_off[GEVO_MAX_PARAMS]; // first cell of writable global param p
@@ -128,10 +130,12 @@ cudaError_t launch_interp(const InterpArgs& A, cudaStream_t stream);
 // Thread-parallel launch shape: warps per CTA and dynamic shared memory, or
 // warps_per_cta == 0 when the instance state does not fit on chip.
 struct TpShape {
-    uint32_t warps_per_cta;
+    uint32_t warps_per_cta; // = simulated threads
+    uint32_t lanes;         // tests per CTA (<= 32)
     size_t smem;
 };
-TpShape tp_shape(uint32_t group, uint32_t max_slots, uint32_t n_cells, uint32_t n_chunks);
+TpShape tp_shape(uint32_t threads, uint32_t n_tests, uint32_t max_slots, uint32_t n_cells,
+                 uint32_t n_chunks);
 cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream);
 cudaError_t launch_error(const uint32_t* cand, const uint32_t* orc, const uint8_t* elem, uint32_t n,
                          double* out, cudaStream_t stream);

@@ -80,8 +80,8 @@ struct DeviceImpl {
 };
 
 struct SuiteImpl {
-    DevBuf param_tag, param_payload, buf_size, buf_elem, setup_code, setup_aux, pool, entry_begin,
-        entries, static_err;
+    DevBuf param_tag, param_payload, buf_size, buf_elem, buf_info, setup_code, setup_aux, pool,
+        entry_begin, entries, static_err;
 };
 
 Device::Device(int ordinal) : impl_(std::make_unique<DeviceImpl>()) {
@@ -148,6 +148,10 @@ DeviceSuite::DeviceSuite(Device& dev, SuiteImage image)
     upload(d.param_payload, image_.param_payload, s);
     upload(d.buf_size, image_.buf_size, s);
     upload(d.buf_elem, image_.buf_elem, s);
+    std::vector<uint32_t> info(image_.buf_size.size());
+    for (size_t i = 0; i < info.size(); ++i)
+        info[i] = (static_cast<uint32_t>(std::max(image_.buf_size[i], 0)) << 8) | image_.buf_elem[i];
+    upload(d.buf_info, info, s);
     upload(d.setup_code, image_.setup_code, s);
     upload(d.setup_aux, image_.setup_aux, s);
     upload(d.pool, image_.pool, s);
@@ -191,6 +195,7 @@ gevo::InterpArgs base_args(DeviceSuite& suite, const ExecImage& ex, const EvalOp
     A.param_payload = d.param_payload.as<uint32_t>();
     A.buf_size = d.buf_size.as<int32_t>();
     A.buf_elem = d.buf_elem.as<uint8_t>();
+    A.buf_info = d.buf_info.as<uint32_t>();
     A.setup_code = d.setup_code.as<uint8_t>();
     A.setup_aux = d.setup_aux.as<int32_t>();
     A.pool = d.pool.as<uint32_t>();
@@ -227,7 +232,7 @@ void bind_batch(gevo::InterpArgs& A, const void* dblob, const gevo_batch_header&
 int64_t spin_threshold() {
     static const int64_t v = [] {
         const char* e = std::getenv("GEVO_SPIN_THRESHOLD");
-        return e ? std::atoll(e) : int64_t(1024);
+        return e ? std::atoll(e) : int64_t(256);
     }();
     return v;
 }
@@ -299,9 +304,7 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
 
     // Thread-parallel lanes (one lane per simulated thread) whenever the
     // instance state fits on chip; the sequential-lane kernel otherwise.
-    uint32_t group = 1;
-    while (group < static_cast<uint32_t>(std::max(ex.threads, 1)))
-        group <<= 1;
+    const uint32_t group = static_cast<uint32_t>(std::max(ex.threads, 1)); // warps per CTA
     uint32_t n_cells = static_cast<uint32_t>(std::max(ex.shared_words, 0));
     for (int p = 0; p < S.n_params; ++p) {
         A.cell_off[p] = n_cells;
@@ -309,18 +312,21 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
             n_cells += static_cast<uint32_t>(S.pool_rows[static_cast<size_t>(p)]);
     }
     const uint32_t n_chunks = std::max<uint32_t>((n_cells + 31) / 32, 1);
-    const gevo::TpShape tps = gevo::tp_shape(group, A.max_slots, n_cells, n_chunks);
-    if (ex.threads >= 1 && ex.threads <= 32 && !opt.want_outputs && !opt.sequential &&
+    const gevo::TpShape tps = gevo::tp_shape(group, T, A.max_slots, n_cells, n_chunks);
+    if (ex.threads >= 1 && !opt.want_outputs && !opt.sequential &&
         tps.warps_per_cta > 0 && tp_enabled()) {
         A.tp_group = group;
+        A.tp_lanes = tps.lanes;
+        const uint32_t tgroups = (T + tps.lanes - 1) / tps.lanes;
         A.n_cells = n_cells;
         A.n_chunks = n_chunks;
         const size_t per_lane = thr > 0 ? 15 * static_cast<size_t>(A.max_slots) + 16 * gevo::kSpinLog
                                         : 0;
-        size_t chunk = std::max<size_t>(dev.scratch_budget / (std::max<size_t>(per_lane, 1) * group * T),
-                                        64);
+        const size_t lanes_per_variant = static_cast<size_t>(tgroups) * 32 * group;
+        size_t chunk = std::max<size_t>(
+            dev.scratch_budget / (std::max<size_t>(per_lane, 1) * lanes_per_variant), 64);
         chunk = std::min<size_t>(chunk, std::max<uint32_t>(h.n_variants, 1));
-        const size_t lanes = chunk * T * group;
+        const size_t lanes = chunk * lanes_per_variant;
         if (thr > 0) {
             reserve_spin(dev, A, lanes);
             A.spin_threshold = thr;
@@ -330,7 +336,7 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
             L.v_begin = static_cast<uint32_t>(vb);
             L.n_var = static_cast<uint32_t>(std::min<uint64_t>(chunk, h.n_variants - vb));
             L.n_inst = L.n_var * T;
-            L.n_spin = L.n_inst * group;
+            L.n_spin = static_cast<uint32_t>(L.n_var * lanes_per_variant);
             check(gevo::launch_interp_tp(L, s), "interp_tp_kernel launch");
             ++launches;
         }

@@ -335,7 +335,7 @@ void BatchImage::add(const Kernel& k) {
         gb.nphi = nphi;
         max_phis = std::max<uint32_t>(max_phis, nphi);
         blocks_.push_back(gb);
-        rel += gb.len;
+        rel += gb.len + 1u; // + fell-off sentinel
     }
     for (const BasicBlock& blk : k.blocks) {
         for (const Instruction& in : blk.instructions) {
@@ -429,6 +429,11 @@ void BatchImage::add(const Kernel& k) {
             }
             insts_.push_back(g);
         }
+        gevo_inst fell{};
+        fell.op = GEVO_OP_FELL;
+        fell.res = GEVO_NO_RESULT;
+        fell.t0 = fell.t1 = -1;
+        insts_.push_back(fell);
     }
     var.n_lits = static_cast<uint16_t>(n_lits);
     var.max_phis = static_cast<uint16_t>(max_phis);
