@@ -554,10 +554,14 @@ __device__ __forceinline__ bool spin_track(const InterpArgs& A, const Lane<kM>& 
             A.sp_log[log_at(A, L, S.nst, 0)] = key;
             A.sp_log[log_at(A, L, S.nst, 1)] = old.x;
             A.sp_log[log_at(A, L, S.nst, 2)] = old.y | vary_store;
-            ++S.nst;
+            hit = S.nst++;
         } else {
             A.sp_log[log_at(A, L, hit, 2)] |= vary_store;
         }
+        // the thread's own last store to the word in the iterate
+        const uint2 sv = L.V(c);
+        A.sp_log[log_at(A, L, hit, 3)] = sv.x;
+        A.sp_log[log_at(A, L, hit, 4)] = sv.y;
         return true;
     }
     case GEVO_OP_BR:
@@ -690,21 +694,28 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
             spin_abandon(S, th, L, 4);
         return;
     }
-    // memory: fixed-value words are back to their S1 contents; no fixed load
-    // reads a word that holds varying data
+    // memory: a word the iterate stores a fixed value to and also reads must
+    // end the iterate with its S1 contents (each iteration then reads the same
+    // value); no load reads a word that holds varying data. Words the iterate
+    // only writes get the same fixed value in every iteration, so skipping
+    // iterations leaves memory as running them would. The comparison uses the
+    // thread's own last store (with thread-parallel lanes a concurrent writer
+    // of the word can only be another thread, whose same-phase write plus this
+    // read is a conflict that re-runs the instance in thread-id order).
     for (uint32_t j = 0; j < S.nst; ++j) {
         const uint32_t key = A.sp_log[log_at(A, L, j, 0)];
         const uint32_t tf = A.sp_log[log_at(A, L, j, 2)];
-        if (tf & 0x100) {
-            for (uint32_t k = 0; k < S.nld; ++k)
-                if (A.sp_ld[log_at(A, L, k, 0)] == key) {
-                    spin_abandon(S, th, L, 7);
-                    return;
-                }
+        bool loaded = false;
+        for (uint32_t k = 0; k < S.nld; ++k)
+            loaded |= A.sp_ld[log_at(A, L, k, 0)] == key;
+        if (!loaded)
             continue;
+        if (tf & 0x100) {
+            spin_abandon(S, th, L, 7);
+            return;
         }
-        const uint2 now = mem_word(A, L, key);
-        if (now.x != A.sp_log[log_at(A, L, j, 1)] || now.y != (tf & 0xFF)) {
+        if (A.sp_log[log_at(A, L, j, 3)] != A.sp_log[log_at(A, L, j, 1)] ||
+            A.sp_log[log_at(A, L, j, 4)] != (tf & 0xFF)) {
             spin_abandon(S, th, L, 8);
             return;
         }
@@ -1425,15 +1436,15 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
 
 // ---- thread-parallel interpreter ---------------------------------------------
 //
-// interp_tp_kernel runs the simulated threads of an instance concurrently on
-// different warps: a CTA holds one variant and up to 32 consecutive tests;
-// warp u runs simulated thread u of every test, lane j test tg * 32 + j. The
-// lanes of a warp execute the same variant and the same thread id on
-// different inputs, so they stay converged like the sequential-lane kernel,
-// while the threads of one instance no longer queue behind each other. The
-// instance's mutable memory -- simulated shared words and its private copies
-// of writable global buffers -- lives in shared-memory cells {payload, tag |
-// writer << 8 | epoch << 16}, one column per test.
+// interp_tp_kernel runs the simulated threads of an instance concurrently. A
+// CTA holds one variant and Ln consecutive tests; lane l of warp w runs
+// simulated thread tid = w * K + l / Ln of test l % Ln (K = 32 / Ln threads per
+// warp). With many tests (the corpus: 8 threads, 16 tests) a warp covers few
+// threads of many tests, whose lanes follow the same path; with many threads
+// and few tests (data-parallel kernels) a warp covers consecutive threads of
+// one test. The instance's mutable memory -- simulated shared words and its
+// private copies of writable global buffers -- lives in shared-memory cells
+// {payload, tag | writer << 8 | epoch << 16}, one column per test.
 //
 // Exactness. Within a phase (the stretch between two barriers) the reference
 // runs threads in id order (src/vm.cpp:121-142), so thread t sees every write
@@ -1457,11 +1468,10 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
 
 namespace {
 
-constexpr uint32_t kTpMaxThreads = 8; // warps per CTA
 enum : uint32_t { kInstPar = 0, kInstSeq = 1, kInstDone = 2 };
-enum : uint32_t { kActContinue = 0, kActFinish = 1, kActRestart = 2 };
+enum : uint32_t { kActContinue = 0, kActFinish = 1, kActRestart = 2, kActNone = 3 };
 
-struct TpShared {
+struct TpInst {
     int32_t min_stop[32];
     uint32_t state[32];
     uint32_t conflict[32];
@@ -1471,25 +1481,29 @@ struct TpShared {
     unsigned long long cost[32];
     unsigned long long ir[32];
     uint32_t jumps[32];
-    uint32_t kind[kTpMaxThreads][32];
-    uint32_t bar[kTpMaxThreads][32];
-    uint32_t tcode[kTpMaxThreads][32];
-    int32_t taux[kTpMaxThreads][32];
-    double err[kTpMaxThreads][32];
 };
 
-// Instance memory cells from the test's inputs; warp u fills words u, u+T, ...
-__device__ __forceinline__ void tp_init_cells(const InterpArgs& A, const Lane<2>& L, uint32_t u,
+struct TpGeom {
+    uint32_t T, Ln, K;
+    // CTA-lane of simulated thread `tid` of test column j
+    __device__ __forceinline__ uint32_t lane_of(uint32_t tid, uint32_t j) const {
+        return (tid / K) * 32 + (tid % K) * Ln + j;
+    }
+};
+
+// Instance memory cells from the test's inputs; thread tid fills words
+// tid, tid + T, ...
+__device__ __forceinline__ void tp_init_cells(const InterpArgs& A, const Lane<2>& L, uint32_t tid,
                                               uint32_t T) {
     const uint32_t SW = static_cast<uint32_t>(max(A.shared_words, 0));
-    for (uint32_t w = u; w < SW; w += T)
+    for (uint32_t w = tid; w < SW; w += T)
         sts2(L.cell(w), 0, GEVO_TAG_UNDEF);
     const size_t tp0 = static_cast<size_t>(L.t) * A.n_params;
     for (uint64_t m = L.writable; m; m &= m - 1) {
         const uint32_t p = static_cast<uint32_t>(__ffsll(static_cast<long long>(m)) - 1);
         const int32_t rows = A.buf_size[tp0 + p];
         const uint32_t elem = A.buf_elem[tp0 + p];
-        for (int32_t e = static_cast<int32_t>(u); e < rows; e += static_cast<int32_t>(T))
+        for (int32_t e = static_cast<int32_t>(tid); e < rows; e += static_cast<int32_t>(T))
             sts2(L.cell(A.cell_off[p] + static_cast<uint32_t>(e)),
                  __ldg(A.pool + A.pool_off[p] + static_cast<size_t>(e) * A.n_tests + L.t), elem);
     }
@@ -1507,37 +1521,50 @@ __device__ __forceinline__ void tp_reset_thread(Lane<2>& L, Thread& th) {
 
 } // namespace
 
-__global__ void __launch_bounds__(256, 2) interp_tp_kernel(const __grid_constant__ InterpArgs A) {
-    __shared__ TpShared S;
-    const uint32_t T = blockDim.x >> 5;            // simulated threads = warps
-    const uint32_t u = threadIdx.x >> 5, j = threadIdx.x & 31;
+__global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_constant__ InterpArgs A) {
+    __shared__ TpInst S;
+    TpGeom G;
+    G.T = static_cast<uint32_t>(A.threads);
+    G.Ln = A.tp_lanes;
+    G.K = 32 / G.Ln;
+    const uint32_t T = G.T, Ln = G.Ln;
+    const uint32_t w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const uint32_t sub = l / Ln, j = l % Ln;
+    const uint32_t tid = w * G.K + sub;
+    const bool lane_ok = sub < G.K && tid < T;
 
     const uint32_t nt = static_cast<uint32_t>(A.n_tests);
-    const uint32_t tgroups = (nt + A.tp_lanes - 1) / A.tp_lanes;
+    const uint32_t tgroups = (nt + Ln - 1) / Ln;
     const uint32_t vl = blockIdx.x / tgroups;
-    const uint32_t t = (blockIdx.x % tgroups) * A.tp_lanes + j;
+    const uint32_t t = (blockIdx.x % tgroups) * Ln + j;
     const uint32_t v = A.v_begin + vl;
-    const bool valid = j < A.tp_lanes && t < nt;
+    const bool inst_ok = t < nt;
+    const bool active = lane_ok && inst_ok;
+    const bool leader = lane_ok && tid == 0;
     const uint64_t gi = static_cast<uint64_t>(v) * nt + t;
 
-    const uint32_t Ln = A.tp_lanes;                // tests (lanes) per CTA
+    // dynamic shared memory: value files | cells | R,W bitsets | per (thread, test)
+    const uint32_t warps = blockDim.x >> 5;
     const uint32_t sbase = smem_addr(g_vfs);
-    const uint32_t cell0 = sbase + T * Ln * A.max_slots * 8;
+    const uint32_t cell0 = sbase + warps * 32 * A.max_slots * 8;
     const uint32_t bits0 = cell0 + Ln * A.n_cells * 8;
     const uint32_t bit_words = A.n_chunks * blockDim.x;
-    uint32_t* bits = reinterpret_cast<uint32_t*>(g_vfs + (T * Ln * A.max_slots + Ln * A.n_cells));
+    const uint32_t Q = T * Ln;
+    const uint32_t pq0 = bits0 + 2 * bit_words * 4;  // kind | bar | tcode | taux (u32 x Q)
+    const uint32_t err0 = (pq0 + 4 * Q * 4 + 7) & ~7u; // err (double x Q)
+    const uint32_t q = tid * Ln + j;
 
     Lane<2> L;
     L.gvf = nullptr;
-    L.vsh = sbase + (u * Ln * A.max_slots + j) * 8;
-    L.vstr = Ln * 8;
+    L.vsh = sbase + (w * 32 * A.max_slots + l) * 8;
+    L.vstr = 32 * 8;
     L.base = 0;
     L.row = 0;
     L.v = v;
-    L.t = valid ? t : 0;
+    L.t = inst_ok ? t : 0;
     L.il = blockIdx.x * 32 + j;
     L.sl = blockIdx.x * blockDim.x + threadIdx.x;
-    L.tid = static_cast<int32_t>(u);
+    L.tid = static_cast<int32_t>(tid);
     L.binfo = A.buf_info + static_cast<size_t>(L.t) * A.n_params;
     L.csh = cell0 + j * 8;
     L.cstr = Ln * 8;
@@ -1559,28 +1586,29 @@ __global__ void __launch_bounds__(256, 2) interp_tp_kernel(const __grid_constant
     L.n_values = 0;
 
     const volatile int32_t* first_fail = A.first_fail;
-    const uint8_t setup = valid ? A.setup_code[t] : GEVO_OK;
-    if (u == 0) {
-        S.cost[j] = 0;
-        S.ir[j] = 0;
-        S.jumps[j] = 0;
-        S.aux[j] = 0;
-        if (!valid) {
-            S.state[j] = kInstDone;
-            S.status[j] = GEVO_STATUS_SKIPPED;
-            S.code[j] = GEVO_SKIPPED;
-        } else if (A.early_exit && first_fail[v] < static_cast<int32_t>(t)) {
-            S.state[j] = kInstDone;
-            S.status[j] = GEVO_STATUS_SKIPPED;
-            S.code[j] = GEVO_SKIPPED;
-        } else if (setup != GEVO_OK) {
+    if (threadIdx.x < 32) {
+        const uint32_t c = threadIdx.x; // instance column
+        const uint32_t tc = (blockIdx.x % tgroups) * Ln + c;
+        S.cost[c] = 0;
+        S.ir[c] = 0;
+        S.jumps[c] = 0;
+        S.aux[c] = 0;
+        S.code[c] = GEVO_OK;
+        if (c >= Ln || tc >= nt) {
+            S.state[c] = kInstDone;
+            S.status[c] = GEVO_STATUS_SKIPPED;
+        } else if (A.early_exit && first_fail[v] < static_cast<int32_t>(tc)) {
+            S.state[c] = kInstDone;
+            S.status[c] = GEVO_STATUS_SKIPPED;
+            S.code[c] = GEVO_SKIPPED;
+        } else if (A.setup_code[tc] != GEVO_OK) {
             // Machine ctor failure: trap with cost 0 (src/vm.cpp:516-520).
-            S.state[j] = kInstDone;
-            S.status[j] = GEVO_STATUS_TRAP;
-            S.code[j] = setup;
-            S.aux[j] = A.setup_aux[t];
+            S.state[c] = kInstDone;
+            S.status[c] = GEVO_STATUS_TRAP;
+            S.code[c] = A.setup_code[tc];
+            S.aux[c] = A.setup_aux[tc];
         } else {
-            S.state[j] = kInstPar;
+            S.state[c] = kInstPar;
         }
     }
     __syncthreads();
@@ -1589,7 +1617,7 @@ __global__ void __launch_bounds__(256, 2) interp_tp_kernel(const __grid_constant
     const uint32_t P = static_cast<uint32_t>(A.n_params);
     Thread th{0, 0, -1, 0, 0, false};
     int64_t cost_commit = 0, ir_commit = 0;
-    if (S.state[j] != kInstDone) {
+    if (active && S.state[j] != kInstDone) {
         L.code = A.insts + var.inst_base;
         L.dblk = A.dblocks + var.block_base;
         L.arm = A.arms + var.arm_base;
@@ -1607,19 +1635,19 @@ __global__ void __launch_bounds__(256, 2) interp_tp_kernel(const __grid_constant
             L.W(lit_begin + k, __ldg(A.lit_payload + var.lit_base + k),
                 __ldg(A.lit_tag + var.lit_base + k));
         tp_reset_thread(L, th);
-        tp_init_cells(A, L, u, T);
+        tp_init_cells(A, L, tid, T);
     }
 
     for (;;) { // phases, CTA-uniform
         ++L.epoch;
-        const uint32_t st = S.state[j];
+        const uint32_t st = active ? S.state[j] : kInstDone;
         if (st == kInstPar) {
             for (uint32_t k = 0; k < A.n_chunks; ++k) {
                 sts1(L.rsh + k * L.bstr, 0);
                 sts1(L.wsh + k * L.bstr, 0);
             }
         }
-        if (u == 0) {
+        if (leader) {
             S.min_stop[j] = INT32_MAX;
             S.conflict[j] = 0;
         }
@@ -1629,96 +1657,100 @@ __global__ void __launch_bounds__(256, 2) interp_tp_kernel(const __grid_constant
             L.seq = false;
             kind = run_thread(A, L, th, first_fail);
             if (kind == kStopTrap)
-                atomicMin(S.min_stop + j, static_cast<int32_t>(u));
+                atomicMin(S.min_stop + j, static_cast<int32_t>(tid));
         }
         if (__syncthreads_or(st == kInstSeq)) {
             // reference schedule: thread after thread, stop at the first trap
-            for (uint32_t w = 0; w < T; ++w) {
-                if (w == u && st == kInstSeq && S.min_stop[j] == INT32_MAX) {
+            for (uint32_t u = 0; u < T; ++u) {
+                if (u == tid && st == kInstSeq && S.min_stop[j] == INT32_MAX) {
                     L.seq = true;
                     kind = run_thread(A, L, th, first_fail);
                     if (kind == kStopTrap)
-                        S.min_stop[j] = static_cast<int32_t>(u);
+                        S.min_stop[j] = static_cast<int32_t>(tid);
                 }
                 __syncthreads();
             }
         }
-        S.kind[u][j] = static_cast<uint32_t>(kind);
-        S.bar[u][j] = th.bar;
-        S.tcode[u][j] = L.code_out;
-        S.taux[u][j] = L.aux;
+        if (lane_ok) {
+            sts1(pq0 + q * 4, static_cast<uint32_t>(kind));
+            sts1(pq0 + (Q + q) * 4, th.bar);
+            sts1(pq0 + (2 * Q + q) * 4, L.code_out);
+            sts1(pq0 + (3 * Q + q) * 4, static_cast<uint32_t>(L.aux));
+        }
         __syncthreads();
         if (st == kInstPar) {
-            // same-phase cross-thread read/write: R_u & W_w, w != u
+            // same-phase cross-thread read/write: R_tid & W_u, u != tid
             uint32_t hit = 0;
             for (uint32_t k = 0; k < A.n_chunks && !hit; ++k) {
                 const uint32_t r = lds1(L.rsh + k * L.bstr);
                 if (!r)
                     continue;
-                for (uint32_t w = 0; w < T; ++w)
-                    if (w != u)
-                        hit |= r & bits[bit_words + k * blockDim.x + w * 32 + j];
+                const uint32_t wk = bits0 + (bit_words + k * blockDim.x) * 4;
+                for (uint32_t u = 0; u < T; ++u)
+                    if (u != tid)
+                        hit |= r & lds1(wk + G.lane_of(u, j) * 4);
             }
             if (hit)
                 S.conflict[j] = 1;
         }
         __syncthreads();
-        // Phase verdict of instance j (every warp derives the same one).
-        uint32_t act = kActContinue, ts = T, status = 0;
-        if (st == kInstDone) {
-            act = kActFinish + 8; // nothing to do
-        } else if (S.conflict[j] || (st == kInstPar && L.epoch >= 0xFFFFu)) {
-            act = kActRestart;
-        } else {
-            for (uint32_t w = 0; w < T; ++w)
-                if (S.kind[w][j] == kStopTrap) {
-                    ts = w;
-                    break;
-                }
-            if (ts < T) {
-                act = kActFinish;
-                const uint32_t c = S.tcode[ts][j];
-                status = c == GEVO_BUDGET_EXCEEDED ? GEVO_STATUS_BUDGET
-                         : c == GEVO_SKIPPED      ? GEVO_STATUS_SKIPPED
-                                                  : GEVO_STATUS_TRAP;
+        // Phase verdict of instance j (every thread of it derives the same one).
+        uint32_t act = kActNone, ts = T, status = 0;
+        if (st != kInstDone) {
+            act = kActContinue;
+            if (S.conflict[j] || (st == kInstPar && L.epoch >= 0xFFFFu)) {
+                act = kActRestart;
             } else {
-                bool all_ret = true, same = true;
-                const uint32_t b0 = S.bar[0][j];
-                for (uint32_t w = 0; w < T; ++w) {
-                    const uint32_t k = S.kind[w][j];
-                    all_ret &= k == kStopRet;
-                    same &= k == kStopSync && S.bar[w][j] == b0;
-                }
-                if (all_ret) {
+                for (uint32_t u = 0; u < T; ++u)
+                    if (lds1(pq0 + (u * Ln + j) * 4) == kStopTrap) {
+                        ts = u;
+                        break;
+                    }
+                if (ts < T) {
                     act = kActFinish;
-                    status = GEVO_STATUS_COMPLETED;
-                } else if (!same) {
-                    act = kActFinish;
-                    status = GEVO_STATUS_TRAP;
-                    ts = T + 1; // divergence
+                    const uint32_t c = lds1(pq0 + (2 * Q + ts * Ln + j) * 4);
+                    status = c == GEVO_BUDGET_EXCEEDED ? GEVO_STATUS_BUDGET
+                             : c == GEVO_SKIPPED      ? GEVO_STATUS_SKIPPED
+                                                      : GEVO_STATUS_TRAP;
+                } else {
+                    bool all_ret = true, same = true;
+                    const uint32_t b0 = lds1(pq0 + (Q + j) * 4);
+                    for (uint32_t u = 0; u < T; ++u) {
+                        const uint32_t k = lds1(pq0 + (u * Ln + j) * 4);
+                        all_ret &= k == kStopRet;
+                        same &= k == kStopSync && lds1(pq0 + (Q + u * Ln + j) * 4) == b0;
+                    }
+                    if (all_ret) {
+                        act = kActFinish;
+                        status = GEVO_STATUS_COMPLETED;
+                    } else if (!same) {
+                        act = kActFinish;
+                        status = GEVO_STATUS_TRAP;
+                        ts = T + 1; // divergence
+                    }
                 }
             }
         }
         __syncthreads(); // verdict inputs read; shared state may change now
         if (act == kActRestart) {
-            if (A.counters && u == 0)
+            if (A.counters && leader)
                 atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 2), 1ull);
             tp_reset_thread(L, th);
-            tp_init_cells(A, L, u, T);
+            tp_init_cells(A, L, tid, T);
             cost_commit = ir_commit = 0;
-            if (u == 0)
+            if (leader)
                 S.state[j] = kInstSeq;
         } else if (act == kActFinish) {
-            const bool mine = ts >= T || u <= ts;
+            const bool mine = ts >= T || tid <= ts;
             atomicAdd(S.cost + j, static_cast<unsigned long long>(mine ? L.cost : cost_commit));
             atomicAdd(S.ir + j, static_cast<unsigned long long>(mine ? L.ir : ir_commit));
             atomicAdd(S.jumps + j, L.jumps);
-            if (u == 0) {
+            if (leader) {
                 S.state[j] = kInstDone;
                 S.status[j] = status;
                 if (ts < T) {
-                    S.code[j] = S.tcode[ts][j];
-                    S.aux[j] = S.taux[ts][j];
+                    S.code[j] = lds1(pq0 + (2 * Q + ts * Ln + j) * 4);
+                    S.aux[j] = static_cast<int32_t>(lds1(pq0 + (3 * Q + ts * Ln + j) * 4));
                 } else if (ts == T + 1) {
                     S.code[j] = GEVO_TRAP_DIVERGENCE;
                     S.aux[j] = 0;
@@ -1732,20 +1764,20 @@ __global__ void __launch_bounds__(256, 2) interp_tp_kernel(const __grid_constant
             cost_commit = L.cost;
             ir_commit = L.ir;
         }
-        if (__syncthreads_and(S.state[j] == kInstDone))
+        if (__syncthreads_and(!active || S.state[j] == kInstDone))
             break;
     }
 
     // compute_error (src/vm.cpp:536-556) of completed instances: max over
-    // oracle elements, spread over the warps (max is order-free).
+    // oracle elements, spread over the instance's threads (max is order-free).
     double worst = 0.0;
-    const bool done_ok = S.status[j] == GEVO_STATUS_COMPLETED;
-    if (done_ok && !A.static_err[t]) {
+    const bool done_ok = inst_ok && S.status[j] == GEVO_STATUS_COMPLETED;
+    if (lane_ok && done_ok && !A.static_err[t]) {
         for (int32_t e = A.entry_begin[t]; e < A.entry_begin[t + 1]; ++e) {
             const OracleEntryDev en = A.entries[e];
             const uint32_t p = static_cast<uint32_t>(en.param);
             const bool priv = (L.writable >> p) & 1ull;
-            for (int32_t k = static_cast<int32_t>(u); k < en.size; k += static_cast<int32_t>(T)) {
+            for (int32_t k = static_cast<int32_t>(tid); k < en.size; k += static_cast<int32_t>(T)) {
                 const uint32_t cw = priv ? lds2(L.cell(A.cell_off[p] + static_cast<uint32_t>(k))).x
                                          : __ldg(A.pool + A.pool_off[p] +
                                                  static_cast<size_t>(k) * nt + t);
@@ -1755,9 +1787,11 @@ __global__ void __launch_bounds__(256, 2) interp_tp_kernel(const __grid_constant
             }
         }
     }
-    S.err[u][j] = worst;
+    double* errs = reinterpret_cast<double*>(reinterpret_cast<char*>(g_vfs) + (err0 - sbase));
+    if (lane_ok)
+        errs[q] = worst;
     __syncthreads();
-    if (u != 0 || !valid)
+    if (!leader || !inst_ok)
         return;
     double error = -1.0;
     if (done_ok) {
@@ -1765,8 +1799,10 @@ __global__ void __launch_bounds__(256, 2) interp_tp_kernel(const __grid_constant
             error = 1.0;
         } else {
             error = 0.0;
-            for (uint32_t w = 0; w < T; ++w)
-                error = (error < S.err[w][j]) ? S.err[w][j] : error;
+            for (uint32_t u = 0; u < T; ++u) {
+                const double e = errs[u * Ln + j];
+                error = (error < e) ? e : error;
+            }
         }
     }
     const uint32_t status = S.status[j];
@@ -1935,24 +1971,35 @@ cudaError_t launch_interp(const InterpArgs& A, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
+size_t tp_smem_bytes(uint32_t threads, uint32_t lanes, uint32_t max_slots, uint32_t n_cells,
+                     uint32_t n_chunks) {
+    const uint32_t K = 32 / lanes;
+    const size_t warps = (threads + K - 1) / K;
+    const size_t Q = static_cast<size_t>(threads) * lanes;
+    size_t b = warps * 32 * max_slots * 8 + static_cast<size_t>(lanes) * n_cells * 8 +
+               2 * static_cast<size_t>(n_chunks) * warps * 32 * 4 + 4 * Q * 4;
+    return ((b + 7) & ~size_t(7)) + Q * 8;
+}
+
 TpShape tp_shape(uint32_t threads, uint32_t n_tests, uint32_t max_slots, uint32_t n_cells,
                  uint32_t n_chunks) {
     TpShape s{0, 0, 0};
-    if (threads < 1 || threads > kTpMaxThreads)
+    if (threads < 1 || threads > kTpMaxBlock)
         return s;
-    // tests per CTA: all of them up to a warp, fewer when the state does not fit
-    for (uint32_t ln = min(max(n_tests, 1u), 32u); ln >= 1; ln = ln > 1 ? (ln + 1) / 2 : 0) {
-        const size_t bytes = static_cast<size_t>(threads) * ln * max_slots * 8 +
-                             static_cast<size_t>(ln) * n_cells * 8 +
-                             2 * static_cast<size_t>(n_chunks) * threads * 32 * 4;
+    // most tests per CTA first (fuller, converged warps), fewer when the
+    // block or its on-chip state would not fit
+    for (uint32_t ln = min(max(n_tests, 1u), 32u); ln >= 1; --ln) {
+        const uint32_t K = 32 / ln;
+        const uint32_t warps = (threads + K - 1) / K;
+        if (warps * 32 > kTpMaxBlock)
+            continue;
+        const size_t bytes = tp_smem_bytes(threads, ln, max_slots, n_cells, n_chunks);
         if (bytes <= kSmemBudget) {
-            s.warps_per_cta = threads;
+            s.warps_per_cta = warps;
             s.lanes = ln;
             s.smem = bytes;
             return s;
         }
-        if (ln == 1)
-            break;
     }
     return s;
 }
@@ -1960,7 +2007,7 @@ TpShape tp_shape(uint32_t threads, uint32_t n_tests, uint32_t max_slots, uint32_
 cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream) {
     if (A.n_inst == 0)
         return cudaSuccess;
-    const TpShape s = tp_shape(A.tp_group, static_cast<uint32_t>(A.n_tests), A.max_slots,
+    const TpShape s = tp_shape(static_cast<uint32_t>(A.threads), static_cast<uint32_t>(A.n_tests), A.max_slots,
                                A.n_cells, A.n_chunks);
     if (s.warps_per_cta == 0 || s.lanes != A.tp_lanes)
         return cudaErrorInvalidConfiguration;

@@ -83,14 +83,14 @@ struct InterpArgs {
     uint32_t* sp_cur;               // stride of the running abstract iterate
     uint8_t* sp_hvary;              // hypothesis: slot may vary (path-irrelevant)
     uint8_t* sp_cvary;              // abstract iterate: slot value is varying
-    uint32_t* sp_log;               // [kSpinLog][inst] x 3: store-log key, old payload, old tag|flags
+    uint32_t* sp_log;               // [kSpinLog][col] x 5: store-log key, old payload,
+                                    // old tag | flags, last stored payload, last stored tag
     uint32_t* sp_ld;                // [kSpinLog][inst] load-log keys
     int64_t spin_threshold;         // per-thread executed count that arms it
     uint32_t n_spin;                // spin scratch columns (instances, or lanes for tp)
 
     // thread-parallel lanes (interp_tp_kernel)
-    uint32_t tp_group;              // simulated threads = warps per CTA (<= 8)
-    uint32_t tp_lanes;              // tests per CTA (lanes used per warp)
+    uint32_t tp_lanes;              // tests per CTA (thread-parallel kernel)
     uint32_t n_cells;               // memory cells per instance: shared words + writable rows
     uint32_t n_chunks;              // 32-bit chunks of a per-lane read / write bitset
     uint32_t cell_off[GEVO_MAX_PARAMS]; // first cell of writable global param p
@@ -108,6 +108,9 @@ constexpr uint32_t kSpinLog = 8;
 
 // Value slots a variant may use (value file in shared memory or global scratch).
 constexpr uint32_t kMaxSlots = GEVO_MAX_SLOTS;
+
+// Largest CTA of the thread-parallel interpreter.
+constexpr uint32_t kTpMaxBlock = 512;
 
 // Shared memory available to the value file of one CTA.
 constexpr size_t kSmemBudget = 200 * 1024;
@@ -130,8 +133,8 @@ cudaError_t launch_interp(const InterpArgs& A, cudaStream_t stream);
 // Thread-parallel launch shape: warps per CTA and dynamic shared memory, or
 // warps_per_cta == 0 when the instance state does not fit on chip.
 struct TpShape {
-    uint32_t warps_per_cta; // = simulated threads
-    uint32_t lanes;         // tests per CTA (<= 32)
+    uint32_t warps_per_cta;
+    uint32_t lanes;         // tests per CTA (<= 32); 32 / lanes simulated threads per warp
     size_t smem;
 };
 TpShape tp_shape(uint32_t threads, uint32_t n_tests, uint32_t max_slots, uint32_t n_cells,

@@ -178,7 +178,7 @@ size_t scratch_per_instance(const SuiteImage& S, uint64_t writable_any, const Ex
     b += 5 * static_cast<size_t>(std::max(ex.shared_words, 0));
     if (any_sync)
         b += static_cast<size_t>(ex.threads) * (4 + 4 + 8 + 4 + 5 * static_cast<size_t>(max_values));
-    b += 15 * static_cast<size_t>(max_slots) + 16 * gevo::kSpinLog; // spin accelerator
+    b += 15 * static_cast<size_t>(max_slots) + 24 * gevo::kSpinLog; // spin accelerator
     if (vf_global)
         b += 8 * static_cast<size_t>(max_slots);
     return b;
@@ -255,7 +255,7 @@ void reserve_spin(DeviceImpl& dev, gevo::InterpArgs& A, size_t cols) {
     dev.sp_cur.reserve(n * 4);
     dev.sp_hvary.reserve(n);
     dev.sp_cvary.reserve(n);
-    dev.sp_log.reserve(cols * gevo::kSpinLog * 3 * 4);
+    dev.sp_log.reserve(cols * gevo::kSpinLog * 5 * 4);
     dev.sp_ld.reserve(cols * gevo::kSpinLog * 4);
     A.sp_hvary = dev.sp_hvary.as<uint8_t>();
     A.sp_cvary = dev.sp_cvary.as<uint8_t>();
@@ -304,7 +304,6 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
 
     // Thread-parallel lanes (one lane per simulated thread) whenever the
     // instance state fits on chip; the sequential-lane kernel otherwise.
-    const uint32_t group = static_cast<uint32_t>(std::max(ex.threads, 1)); // warps per CTA
     uint32_t n_cells = static_cast<uint32_t>(std::max(ex.shared_words, 0));
     for (int p = 0; p < S.n_params; ++p) {
         A.cell_off[p] = n_cells;
@@ -312,17 +311,17 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
             n_cells += static_cast<uint32_t>(S.pool_rows[static_cast<size_t>(p)]);
     }
     const uint32_t n_chunks = std::max<uint32_t>((n_cells + 31) / 32, 1);
-    const gevo::TpShape tps = gevo::tp_shape(group, T, A.max_slots, n_cells, n_chunks);
+    const gevo::TpShape tps =
+        gevo::tp_shape(static_cast<uint32_t>(std::max(ex.threads, 1)), T, A.max_slots, n_cells, n_chunks);
     if (ex.threads >= 1 && !opt.want_outputs && !opt.sequential &&
         tps.warps_per_cta > 0 && tp_enabled()) {
-        A.tp_group = group;
         A.tp_lanes = tps.lanes;
         const uint32_t tgroups = (T + tps.lanes - 1) / tps.lanes;
         A.n_cells = n_cells;
         A.n_chunks = n_chunks;
-        const size_t per_lane = thr > 0 ? 15 * static_cast<size_t>(A.max_slots) + 16 * gevo::kSpinLog
+        const size_t per_lane = thr > 0 ? 15 * static_cast<size_t>(A.max_slots) + 24 * gevo::kSpinLog
                                         : 0;
-        const size_t lanes_per_variant = static_cast<size_t>(tgroups) * 32 * group;
+        const size_t lanes_per_variant = static_cast<size_t>(tgroups) * 32 * tps.warps_per_cta;
         size_t chunk = std::max<size_t>(
             dev.scratch_budget / (std::max<size_t>(per_lane, 1) * lanes_per_variant), 64);
         chunk = std::min<size_t>(chunk, std::max<uint32_t>(h.n_variants, 1));
