@@ -1547,7 +1547,8 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
     const uint32_t warps = blockDim.x >> 5;
     const uint32_t sbase = smem_addr(g_vfs);
     const uint32_t cell0 = sbase + warps * 32 * A.max_slots * 8;
-    const uint32_t bits0 = cell0 + Ln * A.n_cells * 8;
+    const uint32_t back0 = cell0 + Ln * A.n_cells * 8; // phase-start copy of the cells
+    const uint32_t bits0 = back0 + (A.tp_snap ? Ln * A.n_cells * 8 : 0);
     const uint32_t bit_words = A.n_chunks * blockDim.x;
     const uint32_t Q = T * Ln;
     const uint32_t pq0 = bits0 + 2 * bit_words * 4;  // kind | bar | tcode | taux (u32 x Q)
@@ -1616,7 +1617,10 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
     const gevo_variant var = A.variants[v];
     const uint32_t P = static_cast<uint32_t>(A.n_params);
     Thread th{0, 0, -1, 0, 0, false};
+    Thread th_snap = th;
     int64_t cost_commit = 0, ir_commit = 0;
+    bool first_phase = true; // of this instance: a conflict re-runs from the initial state
+    const bool snap = A.tp_snap && (var.flags & GEVO_VAR_HAS_SYNC);
     if (active && S.state[j] != kInstDone) {
         L.code = A.insts + var.inst_base;
         L.dblk = A.dblocks + var.block_base;
@@ -1645,6 +1649,14 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
             for (uint32_t k = 0; k < A.n_chunks; ++k) {
                 sts1(L.rsh + k * L.bstr, 0);
                 sts1(L.wsh + k * L.bstr, 0);
+            }
+            if (snap && !first_phase) {
+                // phase-start state, restored if this phase must run in id order
+                th_snap = th;
+                for (uint32_t x = 0; x < L.n_values; ++x)
+                    A.tp_snap[static_cast<size_t>(x) * A.n_spin + L.sl] = L.V(x);
+                for (uint32_t x = tid; x < A.n_cells; x += T)
+                    sts2(back0 + (x * Ln + j) * 8, lds2(L.cell(x)).x, lds2(L.cell(x)).y);
             }
         }
         if (leader) {
@@ -1735,9 +1747,26 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
         if (act == kActRestart) {
             if (A.counters && leader)
                 atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 2), 1ull);
-            tp_reset_thread(L, th);
-            tp_init_cells(A, L, tid, T);
-            cost_commit = ir_commit = 0;
+            if (first_phase) {
+                tp_reset_thread(L, th);
+                tp_init_cells(A, L, tid, T);
+                cost_commit = ir_commit = 0;
+            } else {
+                // back to the phase start (snap is set: only multi-phase variants get here)
+                th = th_snap;
+                for (uint32_t x = 0; x < L.n_values; ++x) {
+                    const uint2 sv = A.tp_snap[static_cast<size_t>(x) * A.n_spin + L.sl];
+                    L.W(x, sv.x, sv.y);
+                }
+                for (uint32_t x = tid; x < A.n_cells; x += T) {
+                    const uint2 c = lds2(back0 + (x * Ln + j) * 8);
+                    sts2(L.cell(x), c.x, c.y);
+                }
+                L.cost = cost_commit;
+                L.ir = ir_commit;
+                L.code_out = GEVO_OK;
+                L.aux = 0;
+            }
             if (leader)
                 S.state[j] = kInstSeq;
         } else if (act == kActFinish) {
@@ -1763,6 +1792,13 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
             ++th.ip; // step past the barrier
             cost_commit = L.cost;
             ir_commit = L.ir;
+            // the next phase runs concurrently again (a single-phase variant
+            // never continues; a re-run phase 0 has no snapshot to return to)
+            if (snap) {
+                first_phase = false;
+                if (leader)
+                    S.state[j] = kInstPar;
+            }
         }
         if (__syncthreads_and(!active || S.state[j] == kInstDone))
             break;
@@ -1972,17 +2008,17 @@ cudaError_t launch_interp(const InterpArgs& A, cudaStream_t stream) {
 }
 
 size_t tp_smem_bytes(uint32_t threads, uint32_t lanes, uint32_t max_slots, uint32_t n_cells,
-                     uint32_t n_chunks) {
+                     uint32_t n_chunks, bool backup) {
     const uint32_t K = 32 / lanes;
     const size_t warps = (threads + K - 1) / K;
     const size_t Q = static_cast<size_t>(threads) * lanes;
-    size_t b = warps * 32 * max_slots * 8 + static_cast<size_t>(lanes) * n_cells * 8 +
+    size_t b = warps * 32 * max_slots * 8 + static_cast<size_t>(lanes) * n_cells * 8 * (backup ? 2 : 1) +
                2 * static_cast<size_t>(n_chunks) * warps * 32 * 4 + 4 * Q * 4;
     return ((b + 7) & ~size_t(7)) + Q * 8;
 }
 
 TpShape tp_shape(uint32_t threads, uint32_t n_tests, uint32_t max_slots, uint32_t n_cells,
-                 uint32_t n_chunks) {
+                 uint32_t n_chunks, bool backup) {
     TpShape s{0, 0, 0};
     if (threads < 1 || threads > kTpMaxBlock)
         return s;
@@ -1993,7 +2029,7 @@ TpShape tp_shape(uint32_t threads, uint32_t n_tests, uint32_t max_slots, uint32_
         const uint32_t warps = (threads + K - 1) / K;
         if (warps * 32 > kTpMaxBlock)
             continue;
-        const size_t bytes = tp_smem_bytes(threads, ln, max_slots, n_cells, n_chunks);
+        const size_t bytes = tp_smem_bytes(threads, ln, max_slots, n_cells, n_chunks, backup);
         if (bytes <= kSmemBudget) {
             s.warps_per_cta = warps;
             s.lanes = ln;
@@ -2007,8 +2043,8 @@ TpShape tp_shape(uint32_t threads, uint32_t n_tests, uint32_t max_slots, uint32_
 cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream) {
     if (A.n_inst == 0)
         return cudaSuccess;
-    const TpShape s = tp_shape(static_cast<uint32_t>(A.threads), static_cast<uint32_t>(A.n_tests), A.max_slots,
-                               A.n_cells, A.n_chunks);
+    const TpShape s = tp_shape(static_cast<uint32_t>(A.threads), static_cast<uint32_t>(A.n_tests),
+                               A.max_slots, A.n_cells, A.n_chunks, A.tp_snap != nullptr);
     if (s.warps_per_cta == 0 || s.lanes != A.tp_lanes)
         return cudaErrorInvalidConfiguration;
     const unsigned grid = A.n_var * ((static_cast<uint32_t>(A.n_tests) + s.lanes - 1) / s.lanes);

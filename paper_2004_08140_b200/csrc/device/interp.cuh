@@ -91,6 +91,8 @@ struct InterpArgs {
 
     // thread-parallel lanes (interp_tp_kernel)
     uint32_t tp_lanes;              // tests per CTA (thread-parallel kernel)
+    uint2* tp_snap;                 // [value slot][lane] phase-start value files (multi-phase
+                                    // batches; null: conflicts re-run from the initial state)
     uint32_t n_cells;               // memory cells per instance: shared words + writable rows
     uint32_t n_chunks;              // 32-bit chunks of a per-lane read / write bitset
     uint32_t cell_off[GEVO_MAX_PARAMS]; // first cell of writable global param p
@@ -138,7 +140,7 @@ struct TpShape {
     size_t smem;
 };
 TpShape tp_shape(uint32_t threads, uint32_t n_tests, uint32_t max_slots, uint32_t n_cells,
-                 uint32_t n_chunks);
+                 uint32_t n_chunks, bool backup);
 cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream);
 cudaError_t launch_error(const uint32_t* cand, const uint32_t* orc, const uint8_t* elem, uint32_t n,
                          double* out, cudaStream_t stream);

@@ -72,6 +72,7 @@ struct DeviceImpl {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     DevBuf blob, rec, vrec, first_fail, priv, sh_tag, sh_val;
     DevBuf ts_pos, ts_prev, ts_exec, ts_stop, ts_val, ts_tag;
+    DevBuf tp_snap;
     DevBuf bcost, vf, sp_base, sp_btag, sp_delta, sp_cur, sp_hvary, sp_cvary, sp_log, sp_ld,
         counters;
     DevBuf rank;
@@ -312,7 +313,8 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
     }
     const uint32_t n_chunks = std::max<uint32_t>((n_cells + 31) / 32, 1);
     const gevo::TpShape tps =
-        gevo::tp_shape(static_cast<uint32_t>(std::max(ex.threads, 1)), T, A.max_slots, n_cells, n_chunks);
+        gevo::tp_shape(static_cast<uint32_t>(std::max(ex.threads, 1)), T, A.max_slots, n_cells,
+                       n_chunks, h.any_sync != 0);
     if (ex.threads >= 1 && !opt.want_outputs && !opt.sequential &&
         tps.warps_per_cta > 0 && tp_enabled()) {
         A.tp_lanes = tps.lanes;
@@ -329,6 +331,11 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
         if (thr > 0) {
             reserve_spin(dev, A, lanes);
             A.spin_threshold = thr;
+        }
+        A.tp_snap = nullptr;
+        if (h.any_sync) {
+            dev.tp_snap.reserve(lanes * std::max<uint32_t>(h.max_values, 1) * 8);
+            A.tp_snap = dev.tp_snap.as<uint2>();
         }
         for (uint64_t vb = 0; vb < h.n_variants; vb += chunk) {
             gevo::InterpArgs L = A;
