@@ -809,6 +809,35 @@ __device__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Thread& th,
     if (n == 0)
         return true;
     const bool track = S.mode == 2;
+    if (n == 2 && !th.slow && !track) {
+        // loop headers: both arms read before either phi writes (parallel copy)
+        const uint4 r0 = fetch_inst(L.code, b.start), r1 = fetch_inst(L.code, b.start + 1);
+        uint32_t ref0, ref1;
+        uint2 v0, v1;
+        if (!phi_arm(L, r0, th.prev, ref0)) {
+            refund(A, L, th, b, 1);
+            return L.trap(GEVO_TRAP_PHI_NO_INCOMING);
+        }
+        if (!L.fetch(ref0, v0)) {
+            refund(A, L, th, b, 1);
+            return false;
+        }
+        th.ip = 1;
+        if (!phi_arm(L, r1, th.prev, ref1)) {
+            refund(A, L, th, b, 2);
+            return L.trap(GEVO_TRAP_PHI_NO_INCOMING);
+        }
+        if (!L.fetch(ref1, v1)) {
+            refund(A, L, th, b, 2);
+            return false;
+        }
+        th.ip = 2;
+        if (!L.set(f_res(r0), v0.x, v0.y) || !L.set(f_res(r1), v1.x, v1.y)) {
+            refund(A, L, th, b, 2);
+            return false;
+        }
+        return true;
+    }
     if (n == 1) {
         // a single phi reads nothing another phi writes: no staging needed
         const uint4 r = fetch_inst(L.code, b.start);
@@ -1074,7 +1103,34 @@ __device__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th,
             // i32 / f32 arithmetic and compares: both operands carry otag
             const uint2 x = L.V(f_a(r)), y = L.V(f_b(r));
             const uint32_t otag = f_otag(r);
-            if (x.y == otag && y.y == otag) {
+            if (x.y == otag && y.y == otag && op != GEVO_OP_SDIV && op != GEVO_OP_FDIV) {
+                // branch-free: every cheap result is computed, op selects one
+                const float fx = __uint_as_float(x.x), fy = __uint_as_float(y.x);
+                const uint32_t vi = op == GEVO_OP_ADD   ? x.x + y.x
+                                    : op == GEVO_OP_SUB ? x.x - y.x
+                                                        : x.x * y.x;
+                const uint32_t vf = op == GEVO_OP_FADD   ? __float_as_uint(__fadd_rn(fx, fy))
+                                    : op == GEVO_OP_FSUB ? __float_as_uint(__fsub_rn(fx, fy))
+                                                         : __float_as_uint(__fmul_rn(fx, fy));
+                // compares with C++ semantics (NaN: only != holds)
+                const bool icmp = op == GEVO_OP_ICMP;
+                const bool lt = icmp ? static_cast<int32_t>(x.x) < static_cast<int32_t>(y.x) : fx < fy;
+                const bool eq = icmp ? x.x == y.x : fx == fy;
+                const bool gt = icmp ? static_cast<int32_t>(x.x) > static_cast<int32_t>(y.x) : fx > fy;
+                const uint32_t pred = f_aux(r);
+                const bool c = pred == 0 ? eq : pred == 1 ? !eq : pred == 2 ? lt
+                             : pred == 3 ? (lt || eq) : pred == 4 ? gt : (gt || eq);
+                const bool is_cmp = op >= GEVO_OP_ICMP;
+                const uint32_t v = is_cmp ? (c ? 1u : 0u) : (op <= GEVO_OP_MUL ? vi : vf);
+                const uint32_t vt = is_cmp ? static_cast<uint32_t>(GEVO_TAG_BOOL) : otag;
+                const uint32_t res = f_res(r);
+                if (res != GEVO_NO_RESULT) {
+                    L.W(res, v, vt);
+                    ++pc;
+                    continue;
+                }
+                L.trap(GEVO_TRAP_DEF_NO_ID);
+            } else if (x.y == otag && y.y == otag) {
                 uint32_t v;
                 uint32_t vt = otag;
                 ok = true;
