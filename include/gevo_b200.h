@@ -174,6 +174,16 @@ int gevo_benchmark_ir(const char* bench, char** ir);
  * No evaluation: the mix keeps trapping, spinning and over-tolerance
  * variants, as the search's candidate stream does. */
 int gevo_sample_candidates(const char* bench, int n, uint64_t seed, int max_depth, char** patches);
+/* The same for an arbitrary kernel (IR text). */
+int gevo_sample_candidates_ir(const char* kernel_ir, int n, uint64_t seed, int max_depth,
+                              char** patches);
+/* Test suite of an arbitrary kernel from a generator spec document
+ * (src/corpus.cpp generator_spec_from_json + generate_tests_for: seeded
+ * inputs, oracle = the kernel's own outputs, computed on the device). */
+int gevo_suite_from_spec(const char* kernel_ir, const char* gen_json, int n_tests, uint64_t seed,
+                         int device, gevo_suite** out);
+/* Seeded inputs of a generator spec without oracles (TestCase JSON array). */
+int gevo_spec_inputs(const char* gen_json, int count, uint64_t seed, char** tests_json);
 /* Train / held-out suite seeds (src/cli_app.cpp:193-201). */
 uint64_t gevo_train_seed(uint64_t master);
 uint64_t gevo_heldout_seed(uint64_t master);

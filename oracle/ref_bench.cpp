@@ -9,6 +9,11 @@
 //   ref_bench <bench> <variants.txt> <n_tests> <test_seed> <threads> <max_seconds>
 //             [budget=1000000] [tolerance=0]
 //
+// <bench> is a registry name, or file:<prefix> for an authored kernel
+// (<prefix>.ir + <prefix>.gen.json, via the reference's parse_kernel,
+// generator_spec_from_json and generate_tests_for). REF_BENCH_NOCOUNT=1 skips
+// the untimed dynamic-IR counting pass (ir = -1).
+//
 // variants.txt: one patch per line as compact JSON (patch_to_json format).
 // Prints one JSON object: variants, executions (tests actually run, i.e. up to
 // and including the first failing one), ir (reference dynamic instruction
@@ -18,6 +23,8 @@
 #include "evoir/engine.hpp"
 
 #include <atomic>
+#include <cstdlib>
+#include <sstream>
 #include <chrono>
 #include <cstdio>
 #include <fstream>
@@ -32,7 +39,25 @@ int main(int argc, char** argv) {
                      "<max_seconds> [budget] [tolerance]\n";
         return 1;
     }
-    Benchmark b = load_benchmark(argv[1]);
+    const std::string name = argv[1];
+    Kernel kernel;
+    GeneratorSpec gen;
+    bool registry = name.rfind("file:", 0) != 0;
+    Benchmark b;
+    if (registry) {
+        b = load_benchmark(name);
+        kernel = b.kernel;
+    } else {
+        auto slurp = [](const std::string& path) {
+            std::ifstream f(path);
+            std::stringstream ss;
+            ss << f.rdbuf();
+            return ss.str();
+        };
+        const std::string prefix = name.substr(5);
+        kernel = parse_kernel(slurp(prefix + ".ir"));
+        gen = generator_spec_from_json(slurp(prefix + ".gen.json"));
+    }
     std::ifstream in(argv[2]);
     int n_tests = std::stoi(argv[3]);
     uint64_t seed = std::stoull(argv[4]);
@@ -46,10 +71,11 @@ int main(int argc, char** argv) {
     while (std::getline(in, line)) {
         if (line.empty())
             continue;
-        variants.push_back(apply_patch(b.kernel, patch_from_json(line)).kernel);
+        variants.push_back(apply_patch(kernel, patch_from_json(line)).kernel);
     }
-    auto tests = generate_tests(b, n_tests, seed);
-    ExecConfig cfg = ExecConfig::for_kernel(b.kernel);
+    auto tests = registry ? generate_tests(b, n_tests, seed)
+                          : generate_tests_for(kernel, gen, n_tests, seed);
+    ExecConfig cfg = ExecConfig::for_kernel(kernel);
     cfg.instruction_budget = budget;
     ExecConfig unit = cfg;
     {
@@ -61,6 +87,8 @@ int main(int argc, char** argv) {
     std::atomic<size_t> next{0};
     std::atomic<bool> stop{false};
     std::vector<char> done(variants.size(), 0);
+    std::vector<int> ran(variants.size(), 0); // tests evaluate_fitness ran
+    const int n_suite = static_cast<int>(tests.size());
     auto t0 = std::chrono::steady_clock::now();
     auto elapsed = [&] {
         return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -72,8 +100,10 @@ int main(int argc, char** argv) {
                 size_t i = next.fetch_add(1);
                 if (i >= variants.size() || stop.load())
                     return;
-                if (is_valid(variants[i]))
-                    (void)evaluate_fitness(variants[i], tests, cfg, tol);
+                if (is_valid(variants[i])) {
+                    const EvalOutcome o = evaluate_fitness(variants[i], tests, cfg, tol);
+                    ran[i] = o.accepted ? n_suite : o.failing_test + 1;
+                }
                 done[i] = 1;
                 if (elapsed() > max_seconds)
                     stop.store(true);
@@ -85,10 +115,17 @@ int main(int argc, char** argv) {
 
     // Counting pass (untimed): executions and dynamic IR of the same work.
     int64_t execs = 0, ir = 0, processed = 0;
+    const bool count = !std::getenv("REF_BENCH_NOCOUNT");
+    if (!count)
+        ir = -1;
     for (size_t i = 0; i < variants.size(); ++i) {
         if (!done[i])
             continue;
         ++processed;
+        if (!count) {
+            execs += ran[i];
+            continue;
+        }
         if (!is_valid(variants[i]))
             continue;
         for (const auto& t : tests) {

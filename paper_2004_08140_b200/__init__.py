@@ -136,6 +136,11 @@ _SIGNATURES = [
     ("gevo_benchmark_inputs", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _u64, _str_out]),
     ("gevo_benchmark_names", ctypes.c_int, [_str_out]),
     ("gevo_benchmark_ir", ctypes.c_int, [ctypes.c_char_p, _str_out]),
+    ("gevo_sample_candidates_ir", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _u64, ctypes.c_int,
+                                                 _str_out]),
+    ("gevo_suite_from_spec", ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, _u64,
+                                            ctypes.c_int, ctypes.POINTER(_vp)]),
+    ("gevo_spec_inputs", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _u64, _str_out]),
     ("gevo_sample_candidates", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _u64, ctypes.c_int,
                                               _str_out]),
     ("gevo_train_seed", _u64, [_u64]),
@@ -242,6 +247,33 @@ def sample_candidates(bench: str, n: int, seed: int, max_depth: int = 4) -> list
     return [line for line in _take(out).split("\n") if line]
 
 
+def sample_candidates_ir(kernel_ir: str, n: int, seed: int, max_depth: int = 4) -> list:
+    """n validated (not evaluated) mutants of an arbitrary kernel as patch JSON strings."""
+    out = ctypes.c_void_p()
+    _check(lib().gevo_sample_candidates_ir(_b(kernel_ir), n, seed, max_depth, ctypes.byref(out)))
+    return [line for line in _take(out).split("\n") if line]
+
+
+def spec_inputs(gen_json: str, count: int, seed: int) -> list:
+    """Seeded inputs of a generator spec (TestCase JSON documents, no oracles)."""
+    out = ctypes.c_void_p()
+    _check(lib().gevo_spec_inputs(_b(gen_json), count, seed, ctypes.byref(out)))
+    return json.loads(_take(out))
+
+
+KERNEL_DIR = os.path.join(_HERE, "data", "kernels")
+
+
+def authored_kernel(name: str) -> tuple:
+    """(IR text, generator spec JSON) of an authored workload kernel
+    (data/kernels/<name>.ir, <name>.gen.json): svm-rbf (config 3), conv-bn (config 4)."""
+    with open(os.path.join(KERNEL_DIR, name + ".ir")) as f:
+        ir = f.read()
+    with open(os.path.join(KERNEL_DIR, name + ".gen.json")) as f:
+        gen = f.read()
+    return ir, gen
+
+
 def set_stream(stream_ptr: int) -> None:
     """Run the library's launches on a caller's CUDA stream (0 = its own)."""
     _check(lib().gevo_set_stream(ctypes.c_void_p(stream_ptr or None)))
@@ -281,6 +313,16 @@ class Suite:
     def from_benchmark(cls, bench: str, n_tests: int, seed: int, device: int = -1) -> "Suite":
         h = ctypes.c_void_p()
         _check(lib().gevo_suite_from_benchmark(_b(bench), n_tests, seed, device, ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_spec(cls, kernel_ir: str, gen_json: str, n_tests: int, seed: int,
+                  device: int = -1) -> "Suite":
+        """generate_tests_for(kernel, spec, n_tests, seed): seeded inputs, oracle
+        = the kernel's own outputs (computed on the device)."""
+        h = ctypes.c_void_p()
+        _check(lib().gevo_suite_from_spec(_b(kernel_ir), _b(gen_json), n_tests, seed, device,
+                                          ctypes.byref(h)))
         return cls(h)
 
     @classmethod

@@ -472,42 +472,76 @@ int gevo_benchmark_ir(const char* bench, char** ir) {
     return guard([&] { *ir = dup(print_kernel(load_benchmark(bench).kernel)); });
 }
 
+namespace {
+std::string sample_candidates_of(const Kernel& kernel, int n, uint64_t seed, int max_depth) {
+    if (n < 0 || max_depth < 1)
+        throw std::invalid_argument("gevo_sample_candidates: n >= 0 and max_depth >= 1");
+    struct Parent {
+        Kernel k;
+        Patch p;
+    };
+    std::vector<Parent> parents{{kernel, {}}};
+    Rng pick(seed ^ 0xCA7D1DA7E5ULL);
+    std::string out;
+    int made = 0;
+    for (uint64_t i = 0; made < n; ++i) {
+        if (i > static_cast<uint64_t>(n) * 200 + 1000)
+            throw std::invalid_argument("gevo_sample_candidates: kernel yields no valid mutants");
+        const Parent& par = parents[pick.index(parents.size())];
+        Rng rng = Rng::stream(seed, 0xC4, i, 1);
+        const DomTree dom = DomTree::build(par.k);
+        MutationContext ctx(par.k, dom, rng);
+        const MutationResult m = random_mutation(ctx);
+        if (!m)
+            continue;
+        ApplyResult ar = apply_edit(par.k, *m);
+        if (!ar.applied || !is_valid(ar.kernel))
+            continue;
+        Patch p = par.p;
+        p.push_back(*m);
+        out += nlohmann::json::parse(patch_to_json(p)).dump();
+        out += '\n';
+        ++made;
+        if (static_cast<int>(p.size()) < max_depth)
+            parents.push_back({std::move(ar.kernel), std::move(p)});
+    }
+    return out;
+}
+} // namespace
+
 int gevo_sample_candidates(const char* bench, int n, uint64_t seed, int max_depth,
                            char** patches) {
     return guard([&] {
-        if (n < 0 || max_depth < 1)
-            throw std::invalid_argument("gevo_sample_candidates: n >= 0 and max_depth >= 1");
-        const Benchmark b = load_benchmark(bench);
-        struct Parent {
-            Kernel k;
-            Patch p;
-        };
-        std::vector<Parent> parents{{b.kernel, {}}};
-        Rng pick(seed ^ 0xCA7D1DA7E5ULL);
-        std::string out;
-        int made = 0;
-        for (uint64_t i = 0; made < n; ++i) {
-            if (i > static_cast<uint64_t>(n) * 200 + 1000)
-                throw std::invalid_argument("gevo_sample_candidates: kernel yields no valid mutants");
-            const Parent& par = parents[pick.index(parents.size())];
-            Rng rng = Rng::stream(seed, 0xC4, i, 1);
-            const DomTree dom = DomTree::build(par.k);
-            MutationContext ctx(par.k, dom, rng);
-            const MutationResult m = random_mutation(ctx);
-            if (!m)
-                continue;
-            ApplyResult ar = apply_edit(par.k, *m);
-            if (!ar.applied || !is_valid(ar.kernel))
-                continue;
-            Patch p = par.p;
-            p.push_back(*m);
-            out += nlohmann::json::parse(patch_to_json(p)).dump();
-            out += '\n';
-            ++made;
-            if (static_cast<int>(p.size()) < max_depth)
-                parents.push_back({std::move(ar.kernel), std::move(p)});
-        }
-        *patches = dup(out);
+        *patches = dup(sample_candidates_of(load_benchmark(bench).kernel, n, seed, max_depth));
+    });
+}
+
+int gevo_sample_candidates_ir(const char* kernel_ir, int n, uint64_t seed, int max_depth,
+                              char** patches) {
+    return guard([&] {
+        *patches = dup(sample_candidates_of(parse_kernel(kernel_ir), n, seed, max_depth));
+    });
+}
+
+int gevo_suite_from_spec(const char* kernel_ir, const char* gen_json, int n_tests, uint64_t seed,
+                         int device, gevo_suite** out) {
+    return guard([&] {
+        auto s = std::make_unique<gevo_suite>();
+        b200::Device& dev = device_for(device, s->own_device);
+        s->kernel = parse_kernel(kernel_ir);
+        const std::vector<TestCase> tests =
+            generate_tests_for(s->kernel, generator_spec_from_json(gen_json), n_tests, seed);
+        s->suite = std::make_unique<b200::DeviceSuite>(dev, b200::build_suite(s->kernel.params, tests));
+        *out = s.release();
+    });
+}
+
+int gevo_spec_inputs(const char* gen_json, int count, uint64_t seed, char** tests_json) {
+    return guard([&] {
+        nlohmann::json a = nlohmann::json::array();
+        for (const TestCase& t : generate_inputs_for(generator_spec_from_json(gen_json), count, seed))
+            a.push_back(nlohmann::json::parse(testcase_to_json(t)));
+        *tests_json = dup(a.dump());
     });
 }
 

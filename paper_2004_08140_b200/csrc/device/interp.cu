@@ -153,7 +153,8 @@ __device__ __forceinline__ unsigned long long lds64(uint32_t a) {
 template <int kM>
 struct Lane {
     static constexpr bool kSmem = kM >= 1;
-    static constexpr bool kTP = kM == 2;
+    static constexpr bool kTP = kM >= 2;
+    static constexpr bool kGC = kM == 3; // instance memory cells in global memory
     uint32_t vsh;    // kSmem: shared address of slot 0
     uint32_t vstr;   // kSmem: bytes from one slot to the next
     uint2* gvf;      // global value file (kM == 0)
@@ -178,6 +179,10 @@ struct Lane {
     uint32_t rsh, wsh;       // shared addresses of this lane's read / write bitset chunk 0
     uint32_t bstr;           // bytes from one bitset chunk to the next
     uint32_t msh;            // shared address of the instance's min_stop
+    uint32_t fsh;            // shared address of the instance's conflict flag (kGC)
+    uint2* gcell;            // kGC: cell 0 of the instance ([word][instance] in global memory)
+    unsigned long long* gshadow; // kGC: per-word same-phase reader / writer record
+    uint32_t gstr;           // kGC: elements from one word to the next (instances per launch)
     uint32_t epoch;          // phase number (max-tid-wins store rule)
     bool seq;                // sequential fallback: plain stores, no conflict tracking
     // counters
@@ -204,6 +209,30 @@ struct Lane {
     }
     // kTP: shared address of memory cell w of the instance
     __device__ __forceinline__ uint32_t cell(uint32_t w) const { return csh + w * cstr; }
+    // instance memory cell w, wherever it lives
+    __device__ __forceinline__ uint2 cell_get(uint32_t w) const {
+        if (kGC) {
+            // volatile: bypass L1, which the compare-and-swap stores (L2) do not update
+            const unsigned long long v = *reinterpret_cast<const volatile unsigned long long*>(
+                gcell + static_cast<size_t>(w) * gstr);
+            return make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32));
+        }
+        return lds2(cell(w));
+    }
+    __device__ __forceinline__ void cell_put(uint32_t w, uint32_t x, uint32_t y) const {
+        if (kGC)
+            *reinterpret_cast<volatile unsigned long long*>(gcell + static_cast<size_t>(w) * gstr) =
+                (static_cast<unsigned long long>(y) << 32) | x;
+        else
+            sts2(cell(w), x, y);
+    }
+    __device__ __forceinline__ unsigned long long cell_cas(uint32_t w, unsigned long long cmp,
+                                                           unsigned long long val) const {
+        if (kGC)
+            return atomicCAS(reinterpret_cast<unsigned long long*>(gcell + static_cast<size_t>(w) * gstr),
+                             cmp, val);
+        return cas64(cell(w), cmp, val);
+    }
 
     __device__ __forceinline__ bool trap(uint32_t c, int32_t x = 0) {
         code_out = c;
@@ -442,7 +471,7 @@ template <int kM>
 __device__ __forceinline__ uint2 mem_word(const InterpArgs& A, const Lane<kM>& L, uint32_t key) {
     const uint32_t eff = key & 0xFFFFFF, space = key >> 24;
     if (Lane<kM>::kTP) {
-        const uint2 c = lds2(L.cell(space == 0x80 ? eff : A.cell_off[space - 1] + eff));
+        const uint2 c = L.cell_get(space == 0x80 ? eff : A.cell_off[space - 1] + eff);
         return make_uint2(c.x, c.y & 0xFF);
     }
     if (space == 0x80) {
@@ -895,6 +924,46 @@ __device__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Thread& th,
     return true;
 }
 
+// Same-phase access bookkeeping of a thread-parallel lane. Shared-memory
+// cells: per-lane read / write bitsets, checked at the phase end. Global
+// cells: a per-word record {writer epoch, writer, reader epoch, reader}
+// (0xFFFF = several threads) updated with one compare-and-swap; a read and a
+// write of the same word by different threads in one epoch flags the
+// instance right away (the CAS orders them, so one of the two sees the other).
+template <int kM>
+__device__ __forceinline__ void tp_note(const Lane<kM>& L, uint32_t w, bool write) {
+    if (!Lane<kM>::kGC) {
+        const uint32_t ba = (write ? L.wsh : L.rsh) + (w >> 5) * L.bstr;
+        sts1(ba, lds1(ba) | (1u << (w & 31)));
+        return;
+    }
+    unsigned long long* sp = L.gshadow + static_cast<size_t>(w) * L.gstr;
+    const uint32_t me = static_cast<uint32_t>(L.tid), ep = L.epoch & 0xFFFF;
+    unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(sp);
+    for (;;) {
+        uint32_t wr = static_cast<uint32_t>(cur >> 32), rd = static_cast<uint32_t>(cur);
+        uint32_t& mine = write ? wr : rd;
+        const uint32_t other = write ? rd : wr;
+        if ((other >> 16) == ep && (other & 0xFFFF) != me) {
+            sts1(L.fsh, 1u); // same-phase cross-thread read / write
+            return;
+        }
+        uint32_t next = mine;
+        if ((mine >> 16) != ep)
+            next = (ep << 16) | me;
+        else if ((mine & 0xFFFF) != me)
+            next = (ep << 16) | 0xFFFFu;
+        if (next == mine)
+            return;
+        mine = next;
+        const unsigned long long want = (static_cast<unsigned long long>(wr) << 32) | rd;
+        const unsigned long long prev = atomicCAS(sp, cur, want);
+        if (prev == cur)
+            return;
+        cur = prev;
+    }
+}
+
 // Memory instructions (vm.cpp:238-283, 447-460): off the hot dispatch path.
 template <int kM>
 __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const uint4 r) {
@@ -944,14 +1013,10 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
             }
             w = A.cell_off[prm] + static_cast<uint32_t>(eff);
         }
-        const uint32_t ca = L.cell(w);
-        const uint32_t bit = 1u << (w & 31);
         if (op == GEVO_OP_LOAD) {
-            if (!L.seq) {
-                const uint32_t ba = L.rsh + (w >> 5) * L.bstr;
-                sts1(ba, lds1(ba) | bit);
-            }
-            const uint2 x = lds2(ca);
+            if (!L.seq)
+                tp_note(L, w, false);
+            const uint2 x = L.cell_get(w);
             if (p.y == GEVO_TAG_PTR_SHARED) {
                 const uint32_t wt = x.y & 0xFF;
                 if (wt == GEVO_TAG_UNDEF)
@@ -962,25 +1027,23 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
             return L.set(f_res(r), x.x, x.y & 0xFF);
         }
         if (L.seq) {
-            sts2(ca, val.x, val.y);
+            L.cell_put(w, val.x, val.y);
             return true;
         }
-        {
-            const uint32_t ba = L.wsh + (w >> 5) * L.bstr;
-            sts1(ba, lds1(ba) | bit);
-        }
+        tp_note(L, w, true);
         // Same-phase stores of several simulated threads: the highest thread id
         // wins, and a thread's own stores land in program order (the
         // reference runs threads one after another, src/vm.cpp:121-142).
         const uint32_t me = static_cast<uint32_t>(L.tid) + 1;
         const uint32_t meta = val.y | (me << 8) | (L.epoch << 16);
         const unsigned long long want = (static_cast<unsigned long long>(meta) << 32) | val.x;
-        unsigned long long cur = lds64(ca);
+        const uint2 c0 = L.cell_get(w);
+        unsigned long long cur = (static_cast<unsigned long long>(c0.y) << 32) | c0.x;
         for (;;) {
             const uint32_t m = static_cast<uint32_t>(cur >> 32);
             if ((m >> 16) == L.epoch && ((m >> 8) & 0xFF) > me)
                 break;
-            const unsigned long long prev = cas64(ca, cur, want);
+            const unsigned long long prev = L.cell_cas(w, cur, want);
             if (prev == cur)
                 break;
             cur = prev;
@@ -1549,23 +1612,25 @@ struct TpGeom {
 
 // Instance memory cells from the test's inputs; thread tid fills words
 // tid, tid + T, ...
-__device__ __forceinline__ void tp_init_cells(const InterpArgs& A, const Lane<2>& L, uint32_t tid,
+template <int kM>
+__device__ __forceinline__ void tp_init_cells(const InterpArgs& A, const Lane<kM>& L, uint32_t tid,
                                               uint32_t T) {
     const uint32_t SW = static_cast<uint32_t>(max(A.shared_words, 0));
     for (uint32_t w = tid; w < SW; w += T)
-        sts2(L.cell(w), 0, GEVO_TAG_UNDEF);
+        L.cell_put(w, 0, GEVO_TAG_UNDEF);
     const size_t tp0 = static_cast<size_t>(L.t) * A.n_params;
     for (uint64_t m = L.writable; m; m &= m - 1) {
         const uint32_t p = static_cast<uint32_t>(__ffsll(static_cast<long long>(m)) - 1);
         const int32_t rows = A.buf_size[tp0 + p];
         const uint32_t elem = A.buf_elem[tp0 + p];
         for (int32_t e = static_cast<int32_t>(tid); e < rows; e += static_cast<int32_t>(T))
-            sts2(L.cell(A.cell_off[p] + static_cast<uint32_t>(e)),
-                 __ldg(A.pool + A.pool_off[p] + static_cast<size_t>(e) * A.n_tests + L.t), elem);
+            L.cell_put(A.cell_off[p] + static_cast<uint32_t>(e),
+                       __ldg(A.pool + A.pool_off[p] + static_cast<size_t>(e) * A.n_tests + L.t), elem);
     }
 }
 
-__device__ __forceinline__ void tp_reset_thread(Lane<2>& L, Thread& th) {
+template <int kM>
+__device__ __forceinline__ void tp_reset_thread(Lane<kM>& L, Thread& th) {
     for (uint32_t s = 0; s < L.n_values; ++s)
         L.W(s, 0, GEVO_TAG_UNDEF);
     L.cost = 0;
@@ -1577,7 +1642,9 @@ __device__ __forceinline__ void tp_reset_thread(Lane<2>& L, Thread& th) {
 
 } // namespace
 
+template <int kM>
 __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_constant__ InterpArgs A) {
+    constexpr bool kGC = kM == 3; // instance memory in global cells
     __shared__ TpInst S;
     TpGeom G;
     G.T = static_cast<uint32_t>(A.threads);
@@ -1603,15 +1670,16 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
     const uint32_t warps = blockDim.x >> 5;
     const uint32_t sbase = smem_addr(g_vfs);
     const uint32_t cell0 = sbase + warps * 32 * A.max_slots * 8;
-    const uint32_t back0 = cell0 + Ln * A.n_cells * 8; // phase-start copy of the cells
-    const uint32_t bits0 = back0 + (A.tp_snap ? Ln * A.n_cells * 8 : 0);
-    const uint32_t bit_words = A.n_chunks * blockDim.x;
+    const uint32_t smem_cells = kGC ? 0 : A.n_cells;
+    const uint32_t back0 = cell0 + Ln * smem_cells * 8; // phase-start copy of the cells
+    const uint32_t bits0 = back0 + (A.tp_snap ? Ln * smem_cells * 8 : 0);
+    const uint32_t bit_words = kGC ? 0 : A.n_chunks * blockDim.x;
     const uint32_t Q = T * Ln;
     const uint32_t pq0 = bits0 + 2 * bit_words * 4;  // kind | bar | tcode | taux (u32 x Q)
     const uint32_t err0 = (pq0 + 4 * Q * 4 + 7) & ~7u; // err (double x Q)
     const uint32_t q = tid * Ln + j;
 
-    Lane<2> L;
+    Lane<kM> L;
     L.gvf = nullptr;
     L.vsh = sbase + (w * 32 * A.max_slots + l) * 8;
     L.vstr = 32 * 8;
@@ -1629,6 +1697,11 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
     L.wsh = L.rsh + bit_words * 4;
     L.bstr = blockDim.x * 4;
     L.msh = smem_addr(S.min_stop + j);
+    L.fsh = smem_addr(S.conflict + j);
+    const uint32_t il = vl * nt + t; // launch-local instance (global cells)
+    L.gcell = kGC ? A.gcells + il : nullptr;
+    L.gshadow = kGC ? A.gshadow + il : nullptr;
+    L.gstr = A.n_inst;
     L.epoch = 0;
     L.seq = false;
     L.cost = 0;
@@ -1702,11 +1775,12 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
         ++L.epoch;
         const uint32_t st = active ? S.state[j] : kInstDone;
         if (st == kInstPar) {
-            for (uint32_t k = 0; k < A.n_chunks; ++k) {
-                sts1(L.rsh + k * L.bstr, 0);
-                sts1(L.wsh + k * L.bstr, 0);
-            }
-            if (snap && !first_phase) {
+            if (!kGC)
+                for (uint32_t k = 0; k < A.n_chunks; ++k) {
+                    sts1(L.rsh + k * L.bstr, 0);
+                    sts1(L.wsh + k * L.bstr, 0);
+                }
+            if (!kGC && snap && !first_phase) {
                 // phase-start state, restored if this phase must run in id order
                 th_snap = th;
                 for (uint32_t x = 0; x < L.n_values; ++x)
@@ -1746,7 +1820,7 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
             sts1(pq0 + (3 * Q + q) * 4, static_cast<uint32_t>(L.aux));
         }
         __syncthreads();
-        if (st == kInstPar) {
+        if (!kGC && st == kInstPar) {
             // same-phase cross-thread read/write: R_tid & W_u, u != tid
             uint32_t hit = 0;
             for (uint32_t k = 0; k < A.n_chunks && !hit; ++k) {
@@ -1803,7 +1877,7 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
         if (act == kActRestart) {
             if (A.counters && leader)
                 atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 2), 1ull);
-            if (first_phase) {
+            if (first_phase || kGC) {
                 tp_reset_thread(L, th);
                 tp_init_cells(A, L, tid, T);
                 cost_commit = ir_commit = 0;
@@ -1864,13 +1938,16 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
     // oracle elements, spread over the instance's threads (max is order-free).
     double worst = 0.0;
     const bool done_ok = inst_ok && S.status[j] == GEVO_STATUS_COMPLETED;
+    if (!kGC && A.out_cells && lane_ok && done_ok)
+        for (uint32_t x = tid; x < A.n_cells; x += T)
+            A.out_cells[static_cast<size_t>(x) * A.n_inst + il] = L.cell_get(x);
     if (lane_ok && done_ok && !A.static_err[t]) {
         for (int32_t e = A.entry_begin[t]; e < A.entry_begin[t + 1]; ++e) {
             const OracleEntryDev en = A.entries[e];
             const uint32_t p = static_cast<uint32_t>(en.param);
             const bool priv = (L.writable >> p) & 1ull;
             for (int32_t k = static_cast<int32_t>(tid); k < en.size; k += static_cast<int32_t>(T)) {
-                const uint32_t cw = priv ? lds2(L.cell(A.cell_off[p] + static_cast<uint32_t>(k))).x
+                const uint32_t cw = priv ? L.cell_get(A.cell_off[p] + static_cast<uint32_t>(k)).x
                                          : __ldg(A.pool + A.pool_off[p] +
                                                  static_cast<size_t>(k) * nt + t);
                 const uint32_t ow = __ldg(A.pool + en.off + static_cast<size_t>(k) * nt + t);
@@ -2099,16 +2176,26 @@ TpShape tp_shape(uint32_t threads, uint32_t n_tests, uint32_t max_slots, uint32_
 cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream) {
     if (A.n_inst == 0)
         return cudaSuccess;
+    const bool gc = A.gcells != nullptr;
     const TpShape s = tp_shape(static_cast<uint32_t>(A.threads), static_cast<uint32_t>(A.n_tests),
-                               A.max_slots, A.n_cells, A.n_chunks, A.tp_snap != nullptr);
+                               A.max_slots, gc ? 0 : A.n_cells, gc ? 0 : A.n_chunks,
+                               A.tp_snap != nullptr);
     if (s.warps_per_cta == 0 || s.lanes != A.tp_lanes)
         return cudaErrorInvalidConfiguration;
     const unsigned grid = A.n_var * ((static_cast<uint32_t>(A.n_tests) + s.lanes - 1) / s.lanes);
+    if (gc) {
+        const cudaError_t e = cudaFuncSetAttribute(
+            interp_tp_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s.smem));
+        if (e != cudaSuccess)
+            return e;
+        interp_tp_kernel<3><<<grid, 32 * s.warps_per_cta, s.smem, stream>>>(A);
+        return cudaGetLastError();
+    }
     const cudaError_t e = cudaFuncSetAttribute(
-        interp_tp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s.smem));
+        interp_tp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s.smem));
     if (e != cudaSuccess)
         return e;
-    interp_tp_kernel<<<grid, 32 * s.warps_per_cta, s.smem, stream>>>(A);
+    interp_tp_kernel<2><<<grid, 32 * s.warps_per_cta, s.smem, stream>>>(A);
     return cudaGetLastError();
 }
 

@@ -91,6 +91,10 @@ struct InterpArgs {
 
     // thread-parallel lanes (interp_tp_kernel)
     uint32_t tp_lanes;              // tests per CTA (thread-parallel kernel)
+    uint2* gcells;                  // [cell][instance] global instance memory (null: on chip)
+    unsigned long long* gshadow;    // [cell][instance] same-phase access records
+    uint2* out_cells;               // [cell][instance] final memory of completed instances
+                                    // (want_outputs, on-chip cells; null otherwise)
     uint2* tp_snap;                 // [value slot][lane] phase-start value files (multi-phase
                                     // batches; null: conflicts re-run from the initial state)
     uint32_t n_cells;               // memory cells per instance: shared words + writable rows

@@ -72,7 +72,7 @@ struct DeviceImpl {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     DevBuf blob, rec, vrec, first_fail, priv, sh_tag, sh_val;
     DevBuf ts_pos, ts_prev, ts_exec, ts_stop, ts_val, ts_tag;
-    DevBuf tp_snap;
+    DevBuf tp_snap, gcells, gshadow, outcells;
     DevBuf bcost, vf, sp_base, sp_btag, sp_delta, sp_cur, sp_hvary, sp_cvary, sp_log, sp_ld,
         counters;
     DevBuf rank;
@@ -270,9 +270,20 @@ void reserve_spin(DeviceImpl& dev, gevo::InterpArgs& A, size_t cols) {
 
 // Launches the interpreter over all variants in scratch-bounded chunks, then
 // the per-variant reduction. Records land in dev.rec / dev.vrec.
+// Where the final global buffers of the instances are after a launch
+// (want_outputs): the sequential kernel's private copies (u32 words) or the
+// thread-parallel kernel's memory cells (uint2, payload in .x); element e of
+// writable param p of launch-local instance il is at (off[p] + e) * n_inst + il.
+struct OutputWindow {
+    int mode = 0; // 0 none, 1 u32 words, 2 uint2 cells
+    const void* ptr = nullptr;
+    size_t n_inst = 0, words = 0;
+    std::vector<size_t> off;
+};
+
 int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const gevo_batch_header& h,
                uint64_t writable_any, const ExecImage& ex, const EvalOptions& opt,
-               cudaStream_t s) {
+               cudaStream_t s, OutputWindow* ow = nullptr) {
     const SuiteImage& S = suite.image();
     if (h.max_slots > gevo::kMaxSlots)
         throw std::invalid_argument("variant value file exceeds the device limit");
@@ -312,11 +323,15 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
             n_cells += static_cast<uint32_t>(S.pool_rows[static_cast<size_t>(p)]);
     }
     const uint32_t n_chunks = std::max<uint32_t>((n_cells + 31) / 32, 1);
-    const gevo::TpShape tps =
-        gevo::tp_shape(static_cast<uint32_t>(std::max(ex.threads, 1)), T, A.max_slots, n_cells,
-                       n_chunks, h.any_sync != 0);
-    if (ex.threads >= 1 && !opt.want_outputs && !opt.sequential &&
-        tps.warps_per_cta > 0 && tp_enabled()) {
+    const uint32_t threads = static_cast<uint32_t>(std::max(ex.threads, 1));
+    // on-chip instance memory first; global cells when it does not fit
+    gevo::TpShape tps = gevo::tp_shape(threads, T, A.max_slots, n_cells, n_chunks, h.any_sync != 0);
+    bool gc = false;
+    if (tps.warps_per_cta == 0) {
+        tps = gevo::tp_shape(threads, T, A.max_slots, 0, 0, false);
+        gc = tps.warps_per_cta > 0;
+    }
+    if (ex.threads >= 1 && !opt.sequential && tps.warps_per_cta > 0 && tp_enabled()) {
         A.tp_lanes = tps.lanes;
         const uint32_t tgroups = (T + tps.lanes - 1) / tps.lanes;
         A.n_cells = n_cells;
@@ -324,18 +339,43 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
         const size_t per_lane = thr > 0 ? 15 * static_cast<size_t>(A.max_slots) + 24 * gevo::kSpinLog
                                         : 0;
         const size_t lanes_per_variant = static_cast<size_t>(tgroups) * 32 * tps.warps_per_cta;
-        size_t chunk = std::max<size_t>(
-            dev.scratch_budget / (std::max<size_t>(per_lane, 1) * lanes_per_variant), 64);
+        // global cells + access records: 16 bytes per cell per instance
+        const size_t per_variant = std::max<size_t>(per_lane, 1) * lanes_per_variant +
+                                   (gc ? 16 * static_cast<size_t>(n_cells) * T : 0);
+        size_t chunk = std::max<size_t>(dev.scratch_budget / per_variant, 1);
         chunk = std::min<size_t>(chunk, std::max<uint32_t>(h.n_variants, 1));
+        if (opt.want_outputs)
+            chunk = std::max<uint32_t>(h.n_variants, 1); // one launch window
         const size_t lanes = chunk * lanes_per_variant;
         if (thr > 0) {
             reserve_spin(dev, A, lanes);
             A.spin_threshold = thr;
         }
         A.tp_snap = nullptr;
-        if (h.any_sync) {
+        A.out_cells = nullptr;
+        A.gcells = nullptr;
+        A.gshadow = nullptr;
+        if (gc) {
+            const size_t cells = std::max<size_t>(static_cast<size_t>(n_cells) * chunk * T, 1);
+            dev.gcells.reserve(cells * 8);
+            dev.gshadow.reserve(cells * 8);
+            A.gcells = dev.gcells.as<uint2>();
+            A.gshadow = dev.gshadow.as<unsigned long long>();
+        } else if (h.any_sync) {
             dev.tp_snap.reserve(lanes * std::max<uint32_t>(h.max_values, 1) * 8);
             A.tp_snap = dev.tp_snap.as<uint2>();
+        }
+        if (opt.want_outputs && ow) {
+            const size_t n_inst = static_cast<size_t>(h.n_variants) * T;
+            if (!gc) {
+                dev.outcells.reserve(std::max<size_t>(static_cast<size_t>(n_cells) * n_inst * 8, 16));
+                A.out_cells = dev.outcells.as<uint2>();
+            }
+            ow->mode = 2;
+            ow->ptr = gc ? static_cast<const void*>(A.gcells) : static_cast<const void*>(A.out_cells);
+            ow->n_inst = n_inst;
+            ow->words = n_cells;
+            ow->off.assign(A.cell_off, A.cell_off + S.n_params);
         }
         for (uint64_t vb = 0; vb < h.n_variants; vb += chunk) {
             gevo::InterpArgs L = A;
@@ -343,6 +383,10 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
             L.n_var = static_cast<uint32_t>(std::min<uint64_t>(chunk, h.n_variants - vb));
             L.n_inst = L.n_var * T;
             L.n_spin = static_cast<uint32_t>(L.n_var * lanes_per_variant);
+            if (gc)
+                check(cudaMemsetAsync(A.gshadow, 0,
+                                      static_cast<size_t>(n_cells) * L.n_inst * 8, s),
+                      "access records");
             check(gevo::launch_interp_tp(L, s), "interp_tp_kernel launch");
             ++launches;
         }
@@ -398,6 +442,21 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
     if (thr > 0) {
         reserve_spin(dev, A, cap);
         A.spin_threshold = thr;
+    }
+    if (opt.want_outputs && ow) {
+        if (chunk < h.n_variants)
+            throw std::invalid_argument("want_outputs needs a single-launch batch");
+        ow->mode = 1;
+        ow->ptr = dev.priv.ptr;
+        ow->n_inst = static_cast<size_t>(h.n_variants) * T;
+        ow->off.assign(static_cast<size_t>(S.n_params), 0);
+        size_t words = 0;
+        for (int p = 0; p < S.n_params; ++p) {
+            ow->off[static_cast<size_t>(p)] = words;
+            if ((writable_any >> p) & 1ull)
+                words += static_cast<size_t>(S.pool_rows[static_cast<size_t>(p)]);
+        }
+        ow->words = words;
     }
     for (uint64_t vb = 0; vb < h.n_variants; vb += chunk) {
         gevo::InterpArgs L = A;
@@ -455,7 +514,8 @@ EvalResult evaluate(DeviceSuite& suite, BatchImage& batch, const ExecImage& exec
     gevo::InterpArgs A = base_args(suite, exec, opt);
     bind_batch(A, dev.blob.ptr, h);
     check(cudaEventRecord(dev.ev1, s), "event");
-    R.launches = launch_all(dev, suite, A, h, wr, exec, opt, s);
+    OutputWindow ow;
+    R.launches = launch_all(dev, suite, A, h, wr, exec, opt, s, &ow);
     check(cudaEventRecord(dev.ev2, s), "event");
 
     R.variants.resize(h.n_variants);
@@ -474,20 +534,12 @@ EvalResult evaluate(DeviceSuite& suite, BatchImage& batch, const ExecImage& exec
                   "test records D2H");
         R.d2h_bytes += total * sizeof(gevo_test_record);
     }
-    std::vector<uint32_t> priv;
-    size_t chunk = total;
-    if (opt.want_outputs && total) {
-        // Only supported when every instance ran in one launch window.
-        if (R.launches != 3)
-            throw std::invalid_argument("want_outputs needs a single-launch batch");
-        size_t words = 0;
-        for (int p = 0; p < S.n_params; ++p)
-            if ((wr >> p) & 1ull)
-                words += static_cast<size_t>(S.pool_rows[static_cast<size_t>(p)]);
-        priv.resize(words * chunk);
-        if (!priv.empty())
-            check(cudaMemcpyAsync(priv.data(), dev.priv.ptr, priv.size() * 4,
-                                  cudaMemcpyDeviceToHost, s),
+    std::vector<uint32_t> win;
+    const size_t wsz = ow.mode == 2 ? 2 : 1; // u32 per element
+    if (opt.want_outputs && total && ow.mode) {
+        win.resize(ow.words * ow.n_inst * wsz);
+        if (!win.empty())
+            check(cudaMemcpyAsync(win.data(), ow.ptr, win.size() * 4, cudaMemcpyDeviceToHost, s),
                   "outputs D2H");
     }
     check(cudaStreamSynchronize(s), "evaluate");
@@ -504,15 +556,9 @@ EvalResult evaluate(DeviceSuite& suite, BatchImage& batch, const ExecImage& exec
                 if (R.tests[gi].status != GEVO_STATUS_COMPLETED)
                     continue;
                 BufferMap& out = R.outputs[v][static_cast<size_t>(t)];
-                size_t off_words = 0;
                 for (int p = 0; p < S.n_params; ++p) {
                     const Param& prm = S.params[static_cast<size_t>(p)];
-                    const bool global = prm.type.is_ptr() && prm.type.space == MemSpace::Global;
-                    const bool w = (wr >> p) & 1ull;
-                    const size_t region = off_words * chunk;
-                    if (w)
-                        off_words += static_cast<size_t>(S.pool_rows[static_cast<size_t>(p)]);
-                    if (!global)
+                    if (!(prm.type.is_ptr() && prm.type.space == MemSpace::Global))
                         continue;
                     const size_t tp = static_cast<size_t>(t) * S.n_params + p;
                     const int32_t n = S.buf_size[tp];
@@ -521,7 +567,8 @@ EvalResult evaluate(DeviceSuite& suite, BatchImage& batch, const ExecImage& exec
                     const bool mine = (vars[v].writable >> p) & 1ull;
                     for (int32_t e = 0; e < n; ++e) {
                         const uint32_t word =
-                            mine ? priv[region + static_cast<size_t>(e) * chunk + gi]
+                            mine ? win[((ow.off[static_cast<size_t>(p)] + static_cast<size_t>(e)) *
+                                            ow.n_inst + gi) * wsz]
                                  : S.pool[S.pool_off[static_cast<size_t>(p)] +
                                           static_cast<size_t>(e) * S.n_tests + t];
                         if (b.elem == TypeKind::I32) {

@@ -88,6 +88,7 @@ class CTest:
 
     def __init__(self, doc):
         self._keep = []
+        self.words = 0
 
         def bufs(section):
             items = sorted(doc.get(section, {}).items())
@@ -98,6 +99,7 @@ class CTest:
                 else:
                     fmt = "<i" if b["type"] == "i32" else "<f"
                     w = [struct.unpack("<I", struct.pack(fmt, x))[0] for x in b["data"]]
+                self.words += len(w)
                 data = (ctypes.c_uint32 * max(len(w), 1))(*w)
                 nm = name.encode()
                 self._keep += [data, nm]
@@ -135,7 +137,7 @@ STATUS = {0: "completed", 1: "trap", 2: "budget"}
 
 def execute(kernel: Kernel, test: CTest, cfg: Config):
     r = Result()
-    cap = 1 << 16
+    cap = max(1 << 16, test.words + 64)
     words = (ctypes.c_uint32 * cap)()
     offs = (ctypes.c_int32 * 64)()
     sizes = (ctypes.c_int32 * 64)()
