@@ -69,6 +69,15 @@ int gevo_set_stream(void* stream);
  * last reset: out2[0] = budget-bound loops jumped, out2[1] = instructions
  * skipped by those jumps (counted in the records as executed). */
 int gevo_spin_counters(uint64_t* out2, int reset);
+/* Multi-GPU search (one process per GPU): the engine shards
+ * every candidate batch by variant across `world` ranks and exchanges the
+ * 48-byte per-variant records with `fn`, which must all-gather `bytes` from
+ * every rank into `recv` (world * bytes, rank order) -- an NCCL all-gather
+ * over NVLink on a GPU box. world = 1 (the default) disables sharding. No
+ * reference counterpart: the reference's parallel_for (src/engine.cpp:28-62)
+ * is single-process. */
+typedef void (*gevo_allgather_fn)(void* ctx, const void* send, size_t bytes, void* recv);
+int gevo_set_collective(int rank, int world, gevo_allgather_fn fn, void* ctx);
 /* Thread-parallel interpreter counters since the last reset: out2[0] =
  * instances re-executed in thread-id order after a same-phase cross-thread
  * read/write conflict, out2[1] = instances run by the thread-parallel kernel. */

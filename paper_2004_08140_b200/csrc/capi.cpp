@@ -144,6 +144,19 @@ int gevo_spin_counters(uint64_t* out2, int reset) {
     return guard([&] { b200::spin_counters(b200::Device::default_device(), out2, reset != 0); });
 }
 
+int gevo_set_collective(int rank, int world, gevo_allgather_fn fn, void* ctx) {
+    return guard([&] {
+        if (world < 1 || rank < 0 || rank >= world || (world > 1 && !fn))
+            throw std::invalid_argument("gevo_set_collective: bad rank / world / callback");
+        b200::Collective c;
+        c.rank = rank;
+        c.world = world;
+        c.allgather = fn;
+        c.ctx = ctx;
+        b200::set_collective(c);
+    });
+}
+
 int gevo_tp_counters(uint64_t* out2, int reset) {
     return guard([&] { b200::tp_counters(b200::Device::default_device(), out2, reset != 0); });
 }

@@ -110,6 +110,14 @@ __device__ __forceinline__ bool bad_tag(uint32_t t) {
     return t == GEVO_TAG_UNDEF || t == GEVO_TAG_POISON_PARAM || t == GEVO_TAG_POISON_MISSING;
 }
 
+// Branch-free select (the compiler may not re-branch an asm selp).
+__device__ __forceinline__ uint32_t selp(bool p, uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.b32 %0, %1, %2, q;\n\t}"
+        : "=r"(r) : "r"(a), "r"(b), "r"(static_cast<uint32_t>(p)));
+    return r;
+}
+
 // Explicit shared-memory accesses by 32-bit shared-window address: the
 // interpreter's value files and instance memory never go through generic
 // pointers (no per-access window conversion).
@@ -310,6 +318,7 @@ struct Spin {
     int64_t p, c;      // per-iteration instructions / cost
     int64_t H;         // iterations the abstract proof must cover
     int64_t K;         // iterations every compare of the iterate provably keeps its outcome
+    int64_t Koob;      // iterations every strided load provably stays in bounds
     uint32_t nst, nld; // store / load log entries of the abstract iterate
     uint32_t retries;  // abstract iterates re-run with a widened hypothesis
 };
@@ -433,6 +442,28 @@ __device__ int64_t cmp_horizon(int32_t X, int32_t sx, int32_t Y, int32_t sy, uin
     return lo;
 }
 
+// Largest K in [0, H] such that X + k*sx and Y + k*sy stay int32 and their
+// sum stays in [0, size) for every k in [0, K]; -1 when k = 0 already fails.
+__device__ int64_t affine_in_bounds(int32_t X, int32_t sx, int32_t Y, int32_t sy, int32_t size,
+                                    int64_t H) {
+    auto range = [](int64_t v, int64_t s, int64_t h) -> int64_t {
+        if (s > 0)
+            return min(h, (static_cast<int64_t>(INT32_MAX) - v) / s);
+        if (s < 0)
+            return min(h, (v - static_cast<int64_t>(INT32_MIN)) / -s);
+        return h;
+    };
+    H = range(X, sx, range(Y, sy, H));
+    const int64_t e0 = static_cast<int64_t>(X) + Y, st = static_cast<int64_t>(sx) + sy;
+    if (e0 < 0 || e0 >= size)
+        return -1;
+    if (st > 0)
+        return min(H, (static_cast<int64_t>(size) - 1 - e0) / st);
+    if (st < 0)
+        return min(H, e0 / -st);
+    return H;
+}
+
 template <int kM>
 __device__ __forceinline__ uint32_t spin_stride(const InterpArgs& A, const Lane<kM>& L,
                                                 uint32_t s) {
@@ -537,11 +568,31 @@ __device__ __forceinline__ bool spin_track(const InterpArgs& A, const Lane<kM>& 
         break;
     }
     case GEVO_OP_LOAD: case GEVO_OP_STORE: {
-        if (sa | sb | va | vb)
+        if (va | vb)
             return false;
         const uint2 p = L.V(a), i = L.V(b);
         if (!is_ptr_tag(p.y) || i.y != GEVO_TAG_I32)
             return false;
+        if (sa | sb) {
+            // Strided load from a read-only global buffer: the value varies
+            // (path-irrelevant by the other obligations) and the address stays
+            // in bounds for K_oob iterations; the first out-of-bounds
+            // iteration traps for sure, which bounds the jump (trap horizon).
+            if (op != GEVO_OP_LOAD || p.y == GEVO_TAG_PTR_SHARED)
+                return false;
+            const uint32_t prm = p.y & 0x3F;
+            if ((L.writable >> prm) & 1ull)
+                return false;
+            const int32_t size = __ldg(A.buf_size + static_cast<size_t>(L.t) * A.n_params + prm);
+            const int64_t K = affine_in_bounds(static_cast<int32_t>(p.x), static_cast<int32_t>(sa),
+                                               static_cast<int32_t>(i.x), static_cast<int32_t>(sb),
+                                               size, S.Koob);
+            if (K < 0)
+                return false;
+            S.Koob = K;
+            vout = 1;
+            break;
+        }
         const int64_t eff = static_cast<int64_t>(static_cast<int32_t>(p.x)) +
                             static_cast<int32_t>(i.x);
         if (p.y == GEVO_TAG_PTR_SHARED) {
@@ -666,6 +717,7 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
         S.retries = 0;
         S.H = (A.budget - th.executed) / p;
         S.K = S.H;
+        S.Koob = S.H;
         if (S.H < 3) {
             spin_abandon(S, th, L, 4);
             return;
@@ -719,6 +771,7 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
         S.nld = 0;
         S.H = (A.budget - th.executed) / S.p;
         S.K = S.H;
+        S.Koob = S.H;
         if (S.H < 3)
             spin_abandon(S, th, L, 4);
         return;
@@ -749,13 +802,20 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
             return;
         }
     }
-    // Jump n whole iterations. Up to the budget, the record depends on the path
-    // only; a partial jump (a compare flips before the budget runs out) resumes
-    // an execution that may complete, so every value it leaves behind must be
-    // exact: no varying slot, no varying store.
+    // Jump n whole iterations. Iteration k = 0 is the abstract iterate, the jump skips k = 1..n and
+    // interpretation resumes at k = n + 1. With m = min(budget-bound count,
+    // last in-bounds iteration of every strided load), if the path provably
+    // stays fixed through iteration m + 1 (every compare keeps its outcome),
+    // the resumed iteration ends the thread by the budget or an out-of-bounds
+    // trap on the reference's instruction whatever the path-irrelevant
+    // ("varying") values are. Otherwise only a jump up to the first compare
+    // flip is possible, and the execution it resumes may complete, so it needs
+    // exact values everywhere: no varying slot, no varying store.
     const int64_t n_budget = (A.budget - th.executed) / S.p;
-    const int64_t n = min(n_budget, S.K);
-    if (n < n_budget) {
+    const int64_t m = min(n_budget, S.Koob);
+    int64_t n = m;
+    if (S.K < m + 1) {
+        n = S.K;
         bool vary = n < kSpinMinJump;
         for (uint32_t x = 0; x < L.n_values && !vary; ++x)
             vary = A.sp_hvary[sp_at(A, L, x)] != 0;
@@ -786,7 +846,7 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
         }
     }
     S.mode = 0;
-    if (n < n_budget) {
+    if (n < m || S.K < m + 1) {
         // interpret past the flip, then look for the next affine stretch
         S.attempts = 0;
         S.skip = 0;
@@ -1168,24 +1228,31 @@ __device__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th,
             const uint32_t otag = f_otag(r);
             if (x.y == otag && y.y == otag && op != GEVO_OP_SDIV && op != GEVO_OP_FDIV) {
                 // branch-free: every cheap result is computed, op selects one
+                // (selp keeps the compiler from turning the selection back
+                // into a compare-and-branch tree)
                 const float fx = __uint_as_float(x.x), fy = __uint_as_float(y.x);
-                const uint32_t vi = op == GEVO_OP_ADD   ? x.x + y.x
-                                    : op == GEVO_OP_SUB ? x.x - y.x
-                                                        : x.x * y.x;
-                const uint32_t vf = op == GEVO_OP_FADD   ? __float_as_uint(__fadd_rn(fx, fy))
-                                    : op == GEVO_OP_FSUB ? __float_as_uint(__fsub_rn(fx, fy))
-                                                         : __float_as_uint(__fmul_rn(fx, fy));
-                // compares with C++ semantics (NaN: only != holds)
+                const uint32_t add = x.x + y.x, sub = x.x - y.x, mul = x.x * y.x;
+                const uint32_t fad = __float_as_uint(__fadd_rn(fx, fy));
+                const uint32_t fsb = __float_as_uint(__fsub_rn(fx, fy));
+                const uint32_t fml = __float_as_uint(__fmul_rn(fx, fy));
+                // compares with C++ semantics (NaN: only != holds); bit p of
+                // `cm` is the outcome of predicate p (eq ne lt le gt ge)
                 const bool icmp = op == GEVO_OP_ICMP;
                 const bool lt = icmp ? static_cast<int32_t>(x.x) < static_cast<int32_t>(y.x) : fx < fy;
                 const bool eq = icmp ? x.x == y.x : fx == fy;
                 const bool gt = icmp ? static_cast<int32_t>(x.x) > static_cast<int32_t>(y.x) : fx > fy;
-                const uint32_t pred = f_aux(r);
-                const bool c = pred == 0 ? eq : pred == 1 ? !eq : pred == 2 ? lt
-                             : pred == 3 ? (lt || eq) : pred == 4 ? gt : (gt || eq);
+                const uint32_t cm = static_cast<uint32_t>(eq) | (static_cast<uint32_t>(!eq) << 1) |
+                                    (static_cast<uint32_t>(lt) << 2) |
+                                    (static_cast<uint32_t>(lt || eq) << 3) |
+                                    (static_cast<uint32_t>(gt) << 4) |
+                                    (static_cast<uint32_t>(gt || eq) << 5);
+                const uint32_t c = (cm >> f_aux(r)) & 1u;
+                const uint32_t o3 = op & 3u; // add/fadd 0, sub/fsub 1, mul/fmul 2
+                const uint32_t vi = selp(o3 == 0, add, selp(o3 == 1, sub, mul));
+                const uint32_t vf = selp(o3 == 0, fad, selp(o3 == 1, fsb, fml));
                 const bool is_cmp = op >= GEVO_OP_ICMP;
-                const uint32_t v = is_cmp ? (c ? 1u : 0u) : (op <= GEVO_OP_MUL ? vi : vf);
-                const uint32_t vt = is_cmp ? static_cast<uint32_t>(GEVO_TAG_BOOL) : otag;
+                const uint32_t v = selp(is_cmp, c, selp(op <= GEVO_OP_MUL, vi, vf));
+                const uint32_t vt = selp(is_cmp, static_cast<uint32_t>(GEVO_TAG_BOOL), otag);
                 const uint32_t res = f_res(r);
                 if (res != GEVO_NO_RESULT) {
                     L.W(res, v, vt);
@@ -1657,9 +1724,12 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
     const bool lane_ok = sub < G.K && tid < T;
 
     const uint32_t nt = static_cast<uint32_t>(A.n_tests);
-    const uint32_t tgroups = (nt + Ln - 1) / Ln;
-    const uint32_t vl = blockIdx.x / tgroups;
-    const uint32_t t = (blockIdx.x % tgroups) * Ln + j;
+    // test groups major: every variant's first tests are scheduled before any
+    // later ones, so the early-exit protocol (first_fail) can skip the tests
+    // the reference never runs after a failure
+    const uint32_t vl = blockIdx.x % A.n_var;
+    const uint32_t tg = blockIdx.x / A.n_var;
+    const uint32_t t = tg * Ln + j;
     const uint32_t v = A.v_begin + vl;
     const bool inst_ok = t < nt;
     const bool active = lane_ok && inst_ok;
@@ -1718,7 +1788,7 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
     const volatile int32_t* first_fail = A.first_fail;
     if (threadIdx.x < 32) {
         const uint32_t c = threadIdx.x; // instance column
-        const uint32_t tc = (blockIdx.x % tgroups) * Ln + c;
+        const uint32_t tc = tg * Ln + c;
         S.cost[c] = 0;
         S.ir[c] = 0;
         S.jumps[c] = 0;

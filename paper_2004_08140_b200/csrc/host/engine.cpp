@@ -76,6 +76,11 @@ void host_parallel(size_t n, int jobs, const std::function<void(size_t)>& fn) {
         std::rethrow_exception(err);
 }
 
+b200::Collective& collective_slot() {
+    static b200::Collective c;
+    return c;
+}
+
 double ms_since(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -87,6 +92,8 @@ int wave_size(int used, int retries) {
 }
 
 // Device verdicts for a list of kernels (no validation; evaluate_fitness).
+// With a multi-rank collective, rank r evaluates the contiguous shard
+// [begin_r, end_r) of the batch and the records are all-gathered.
 std::vector<EvalOutcome> device_verdicts(b200::DeviceSuite& suite, const b200::ExecImage& ex,
                                          const std::vector<const Kernel*>& ks, double tol,
                                          bool with_reasons, EngineCounters& ctr) {
@@ -98,19 +105,45 @@ std::vector<EvalOutcome> device_verdicts(b200::DeviceSuite& suite, const b200::E
             o = EvalOutcome::rejected(-1, "no test cases");
         return out;
     }
+    const b200::Collective& col = b200::collective();
+    const bool shard = col.world > 1 && col.allgather && !with_reasons;
+    const size_t n = ks.size(), W = shard ? static_cast<size_t>(col.world) : 1;
+    const size_t R = shard ? static_cast<size_t>(col.rank) : 0;
+    auto span = [&](size_t r) {
+        const size_t q = n / W, m = n % W;
+        const size_t b = r * q + std::min(r, m);
+        return std::make_pair(b, b + q + (r < m ? 1 : 0));
+    };
+    const auto [lo, hi] = span(R);
     b200::BatchImage batch(suite.image());
-    for (const Kernel* k : ks)
-        batch.add(*k);
+    for (size_t v = lo; v < hi; ++v)
+        batch.add(*ks[v]);
     b200::EvalOptions opt;
     opt.tolerance = tol;
     opt.early_exit = true;
-    const b200::EvalResult r = b200::evaluate(suite, batch, ex, opt);
+    b200::EvalResult r;
+    if (hi > lo)
+        r = b200::evaluate(suite, batch, ex, opt);
+    std::vector<gevo_variant_record> recs;
+    if (shard) {
+        const size_t m = (n + W - 1) / W;
+        std::vector<gevo_variant_record> send(m), recv(m * W);
+        std::copy(r.variants.begin(), r.variants.end(), send.begin());
+        col.allgather(col.ctx, send.data(), m * sizeof(gevo_variant_record), recv.data());
+        recs.reserve(n);
+        for (size_t q = 0; q < W; ++q) {
+            const auto [b, e] = span(q);
+            recs.insert(recs.end(), recv.begin() + q * m, recv.begin() + q * m + (e - b));
+        }
+    } else {
+        recs = std::move(r.variants);
+    }
     ctr.candidates += static_cast<int64_t>(ks.size());
     ctr.launches += r.launches;
     ctr.batches += 1;
     ctr.device_ms += r.kernel_ms;
     for (size_t v = 0; v < ks.size(); ++v) {
-        const gevo_variant_record& x = r.variants[v];
+        const gevo_variant_record& x = recs[v];
         ctr.executions += x.execs_ref;
         ctr.dynamic_ir += x.ir_ref;
         if (x.accepted) {
@@ -128,6 +161,11 @@ std::vector<EvalOutcome> device_verdicts(b200::DeviceSuite& suite, const b200::E
 }
 
 } // namespace
+
+namespace b200 {
+void set_collective(const Collective& c) { collective_slot() = c; }
+const Collective& collective() { return collective_slot(); }
+} // namespace b200
 
 // ---------------------------------------------------------------------------
 // Speculation state

@@ -91,6 +91,21 @@ void spin_counters(Device& dev, uint64_t out[2], bool reset);
 // after a same-phase cross-thread conflict, instances run}.
 void tp_counters(Device& dev, uint64_t out[2], bool reset);
 
+// Multi-GPU exchange: one process per GPU; the engine shards
+// each candidate batch across the ranks by variant and all-gathers the
+// fixed-size per-variant records. `allgather` receives `bytes` from every
+// rank into `recv` in rank order (NCCL over NVLink on a GPU box, gloo in CPU
+// tests); the host work around it is replicated, so every rank keeps an
+// identical search state.
+struct Collective {
+    int rank = 0;
+    int world = 1;
+    void (*allgather)(void* ctx, const void* send, size_t bytes, void* recv) = nullptr;
+    void* ctx = nullptr;
+};
+void set_collective(const Collective& c);
+const Collective& collective();
+
 // GPU NSGA ranking (front + crowding + fronts in reference order).
 ParetoRank rank_on_device(Device& dev, const std::vector<FitnessVector>& fits, bool single_group);
 

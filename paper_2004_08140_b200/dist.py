@@ -71,3 +71,46 @@ def accepted_fitness(gathered: np.ndarray) -> tuple:
     keep = gathered[:, 2] > 0.5
     idx = np.nonzero(keep)[0]
     return gathered[keep, 0], gathered[keep, 1], idx
+
+
+# ctypes type of gevo_allgather_fn (include/gevo_b200.h)
+_ALLGATHER_FN = None
+_installed = []
+
+
+def install_collective(device=None, group=None):
+    """Route the engine's record exchange through torch.distributed: every
+    candidate batch of run_search is then sharded by variant across the
+    process group's ranks and the 48-byte records are all-gathered (NCCL over
+    NVLink when the group is NCCL and `device` a CUDA device, gloo on CPU)."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from . import lib, _check
+
+    global _ALLGATHER_FN
+    if _ALLGATHER_FN is None:
+        _ALLGATHER_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                         ctypes.c_void_p)
+    world = dist.get_world_size(group)
+    dev = torch.device("cpu") if device is None else torch.device(device)
+
+    def gather(_ctx, send, nbytes, recv):
+        src = (ctypes.c_uint8 * nbytes).from_address(send)
+        t = torch.frombuffer(bytearray(src), dtype=torch.uint8).to(dev)
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t, group=group)
+        flat = torch.cat(out).cpu().numpy()
+        ctypes.memmove(recv, flat.ctypes.data, flat.nbytes)
+
+    cb = _ALLGATHER_FN(gather)
+    _installed.append(cb)  # keep the trampoline alive
+    _check(lib().gevo_set_collective(dist.get_rank(group), world, ctypes.cast(cb, ctypes.c_void_p),
+                                     None))
+
+
+def uninstall_collective():
+    from . import lib, _check
+    _check(lib().gevo_set_collective(0, 1, None, None))

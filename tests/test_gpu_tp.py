@@ -129,6 +129,25 @@ entry:
   store out[%0], %5  #uid=9
   ret  #uid=10
 }""",
+    # strided reads of a read-only buffer until they leave it: the spin
+    # accelerator jumps to the iteration before the out-of-bounds load
+    "stream_until_oob": """kernel k(a: ptr<global> f32, out: ptr<global> f32) threads=8 shared=0 {
+entry:
+  %0 = tid i32  #uid=0
+  %1 = mul i32 %0, 1000  #uid=1
+  br loop  #uid=2
+loop:
+  %2 = phi i32 [%1, entry], [%6, loop]  #uid=3
+  %3 = phi f32 [0.0, entry], [%5, loop]  #uid=4
+  %4 = load f32 a[%2]  #uid=5
+  %5 = fadd f32 %3, %4  #uid=6
+  %6 = add i32 %2, 3  #uid=7
+  %7 = icmp.ne i32 %6, -5  #uid=8
+  br %7, loop, done  #uid=9
+done:
+  store out[%0], %5  #uid=10
+  ret  #uid=11
+}""",
 }
 
 
@@ -139,6 +158,9 @@ def test_tp_stop_and_race_schedules_match_oracle(gevo, name):
     zero = 0 if elem == "i32" else 0.0
     doc = {"inputs": {"out": {"type": elem, "data": [zero] * 8}}, "scalars": {}, "oracle": {}}
     budget = 20000
+    if "a: ptr<global>" in ir:
+        doc["inputs"]["a"] = {"type": "f32", "data": [0.5] * 30000}
+        budget = 200000
     k = ob.Kernel(ir)
     ocfg = ob.config(8, 8 if "shared=8" in ir else 0, budget)
     exp = ob.execute(k, ob.CTest(doc), ocfg)
