@@ -18,7 +18,7 @@ from typing import Iterable, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgevo_b200.so")
+LIB_PATH = os.environ.get("GEVO_LIB") or os.path.join(_HERE, "libgevo_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "gevo_b200.h")
 
 # ---- record layouts (bytecode.h) ---------------------------------------------

@@ -321,6 +321,7 @@ struct Spin {
     int64_t Koob;      // iterations every strided load provably stays in bounds
     uint32_t nst, nld; // store / load log entries of the abstract iterate
     uint32_t retries;  // abstract iterates re-run with a widened hypothesis
+    int32_t avoid;     // block not to take as the next anchor (-1: none)
 };
 
 template <int kM>
@@ -388,10 +389,19 @@ __device__ __forceinline__ size_t sp_at(const InterpArgs& A, const Lane<kM>& L, 
 template <int kM>
 __device__ __forceinline__ void spin_abandon(Spin& S, const Thread& th, Lane<kM>& L,
                                              uint32_t why) {
-    S.mode = 0;
     ++S.attempts;
     S.skip = S.attempts & 3u;
     S.next = S.attempts > 12 ? INT64_MAX : th.executed + (th.executed >> 1) + 64;
+    if (S.mode == 2 && S.K < S.H && S.attempts <= 12) {
+        // The anchor's loop leaves its path within K + 1 iterations (an inner
+        // loop running out): try again right after that, at a block other
+        // than this anchor -- typically the enclosing loop, whose iterations
+        // repeat with a fixed path.
+        S.next = S.e0 + (S.K + 1) * S.p + 1;
+        S.skip = 0;
+        S.avoid = S.anchor;
+    }
+    S.mode = 0;
     L.spin_dbg = why;
 }
 
@@ -554,9 +564,9 @@ __device__ __forceinline__ bool spin_track(const InterpArgs& A, const Lane<kM>& 
             const int64_t K = cmp_horizon(static_cast<int32_t>(x.x), static_cast<int32_t>(sa),
                                           static_cast<int32_t>(y.x), static_cast<int32_t>(sb),
                                           f_aux(r), S.K);
+            S.K = K;
             if (K < kSpinMinJump)
                 return false;
-            S.K = K;
         }
         break;
     case GEVO_OP_SELECT: {
@@ -665,6 +675,8 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
             --S.skip;
             return;
         }
+        if (th.block == S.avoid)
+            return;
         for (uint32_t x = 0; x < L.n_values; ++x) {
             const uint2 v = L.V(x);
             A.sp_base[sp_at(A, L, x)] = v.x;
@@ -1197,6 +1209,8 @@ __device__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th,
     S.skip = 0;
     S.attempts = 0;
     S.next = A.sp_base ? A.spin_threshold : INT64_MAX;
+    S.avoid = -1;
+    S.K = S.H = 0;
     int64_t bcost;
     Blk b = load_blk(L.dblk, th.block, bcost);
     charge_block(A, L, th, b, bcost, static_cast<uint32_t>(th.ip));
@@ -1226,6 +1240,7 @@ __device__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th,
             // i32 / f32 arithmetic and compares: both operands carry otag
             const uint2 x = L.V(f_a(r)), y = L.V(f_b(r));
             const uint32_t otag = f_otag(r);
+#ifdef GEVO_ARITH_SELP // branch-free variant (faster in the sequential kernel alone, slower overall)
             if (x.y == otag && y.y == otag && op != GEVO_OP_SDIV && op != GEVO_OP_FDIV) {
                 // branch-free: every cheap result is computed, op selects one
                 // (selp keeps the compiler from turning the selection back
@@ -1260,7 +1275,9 @@ __device__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th,
                     continue;
                 }
                 L.trap(GEVO_TRAP_DEF_NO_ID);
-            } else if (x.y == otag && y.y == otag) {
+            } else
+#endif
+            if (x.y == otag && y.y == otag) {
                 uint32_t v;
                 uint32_t vt = otag;
                 ok = true;
