@@ -172,6 +172,8 @@ typedef struct {
     uint32_t max_slots;   /* max n_slots over variants */
     uint32_t max_values;
     uint32_t any_sync;
+    uint32_t max_lits;    /* max n_lits over variants */
+    uint32_t max_lane_slots; /* max n_values + max_phis over variants */
     uint32_t pad;
     /* byte offsets of each section from the start of the blob */
     uint64_t off_variants, off_blocks, off_insts, off_arms, off_lit_payload, off_lit_tag;
@@ -179,7 +181,7 @@ typedef struct {
 } gevo_batch_header;
 
 #define GEVO_MAGIC 0x4F564547u
-#define GEVO_VERSION 3u
+#define GEVO_VERSION 4u
 
 /* Per-(variant, test) record written by the interpreter. */
 typedef struct {

@@ -118,6 +118,15 @@ __device__ __forceinline__ uint32_t selp(bool p, uint32_t a, uint32_t b) {
     return r;
 }
 
+// Thread-parallel value files: CTA-shared parameter / literal tables (less
+// shared memory per lane, one more address decision per operand) or every
+// slot in the lane's own file.
+#ifdef GEVO_TP_TABLES
+constexpr bool kTpTables = true;
+#else
+constexpr bool kTpTables = false;
+#endif
+
 // Explicit shared-memory accesses by 32-bit shared-window address: the
 // interpreter's value files and instance memory never go through generic
 // pointers (no per-access window conversion).
@@ -165,6 +174,13 @@ struct Lane {
     static constexpr bool kGC = kM == 3; // instance memory cells in global memory
     uint32_t vsh;    // kSmem: shared address of slot 0
     uint32_t vstr;   // kSmem: bytes from one slot to the next
+    // kTP: only SSA values and phi staging live in the lane's value file; the
+    // parameters (per test) and literals (per variant) are CTA-shared tables
+    uint32_t nv;     // kTP: n_values (slots below: lane value file)
+    uint32_t tsh;    // kTP: shared address of this test's parameter entry 0
+    uint32_t tstr;   // kTP: bytes between parameter entries
+    uint32_t lsh;    // kTP: shared address of literal 0 (slot lit_begin)
+    uint32_t lit_begin;
     uint2* gvf;      // global value file (kM == 0)
     uint32_t base;   // element index of slot 0
     uint32_t row;
@@ -204,13 +220,28 @@ struct Lane {
     uint32_t code_out;
     int32_t aux;
 
+    // kTP slot -> shared address: values, then params + poison (per test),
+    // literals (per variant), then phi staging back in the lane's file
+    __device__ __forceinline__ uint32_t tp_addr(uint32_t s) const {
+        if (s < nv)
+            return vsh + s * vstr;
+        if (s < lit_begin)
+            return tsh + (s - nv) * tstr;
+        if (s < stage_base)
+            return lsh + (s - lit_begin) * 8;
+        return vsh + (nv + s - stage_base) * vstr;
+    }
     __device__ __forceinline__ uint2 V(uint32_t s) const {
+        if (kTP && kTpTables)
+            return lds2(tp_addr(s));
         if (kSmem)
             return lds2(vsh + s * vstr);
         return gvf[base + s * row];
     }
     __device__ __forceinline__ void W(uint32_t s, uint32_t payload, uint32_t tag) {
-        if (kSmem)
+        if (kTP && kTpTables)
+            sts2(tp_addr(s), payload, tag);
+        else if (kSmem)
             sts2(vsh + s * vstr, payload, tag);
         else
             gvf[base + s * row] = make_uint2(payload, tag);
@@ -324,13 +355,20 @@ struct Spin {
     int32_t avoid;     // block not to take as the next anchor (-1: none)
 };
 
-template <int kM>
-__device__ __noinline__ int64_t suffix_cost(const InterpArgs& A, const Lane<kM>& L, const Blk& b,
-                                            uint32_t from) {
+// Cost of instructions [from, len) of a block (scalar arguments only: a
+// reference to the lane would force it into local memory).
+__device__ __noinline__ int64_t suffix_cost_of(const int64_t* cost, const gevo_inst* code,
+                                               uint32_t start, uint32_t len, uint32_t from) {
     int64_t c = 0;
-    for (uint32_t j = from; j < b.len; ++j)
-        c += A.cost[__ldg(reinterpret_cast<const uint32_t*>(L.code + b.start + j)) >> 24];
+    for (uint32_t j = from; j < len; ++j)
+        c += cost[__ldg(reinterpret_cast<const uint32_t*>(code + start + j)) >> 24];
     return c;
+}
+
+template <int kM>
+__device__ __forceinline__ int64_t suffix_cost(const InterpArgs& A, const Lane<kM>& L, const Blk& b,
+                                               uint32_t from) {
+    return suffix_cost_of(A.cost, L.code, b.start, b.len, from);
 }
 
 // Charges instructions [from, len) of the current block on entry / resume.
@@ -898,7 +936,7 @@ __device__ __forceinline__ bool phi_arm(const Lane<kM>& L, const uint4 r, int32_
 
 // enter_block (vm.cpp:293-333): charge and stage every leading phi, then write.
 template <int kM>
-__device__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Thread& th,
+__device__ __forceinline__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Thread& th,
                             int32_t target, Blk& b, Spin& S) {
     th.prev = th.block;
     th.block = target;
@@ -1202,7 +1240,7 @@ __device__ __forceinline__ bool misc_op(const InterpArgs& A, Lane<kM>& L, const 
 // run_to_barrier (vm.cpp:340-387) + step (389-482) for one simulated thread
 // from (th.block, th.ip). Returns kStopRet, kStopSync or kStopTrap.
 template <int kM>
-__device__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th,
+__device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th,
                           const volatile int32_t* first_fail) {
     Spin S;
     S.mode = 0;
@@ -1407,7 +1445,7 @@ __device__ __forceinline__ void reset_values(Lane<kM>& L) {
 
 // Machine::run for one instance (src/vm.cpp:114-150). Returns the status.
 template <int kM>
-__device__ uint32_t run_instance(const InterpArgs& A, Lane<kM>& L, const gevo_variant& var,
+__device__ __forceinline__ uint32_t run_instance(const InterpArgs& A, Lane<kM>& L, const gevo_variant& var,
                                  const volatile int32_t* first_fail) {
     const int32_t T = A.threads;
     if (!(var.flags & GEVO_VAR_HAS_SYNC)) {
@@ -1504,7 +1542,7 @@ __device__ uint32_t run_instance(const InterpArgs& A, Lane<kM>& L, const gevo_va
 // over oracle elements of the clamped relative difference. max() is exact and
 // order-free, so the per-buffer early return of the reference is not needed.
 template <int kM>
-__device__ double instance_error(const InterpArgs& A, const Lane<kM>& L) {
+__device__ __forceinline__ double instance_error(const InterpArgs& A, const Lane<kM>& L) {
     if (A.static_err[L.t])
         return 1.0;
     const uint32_t nt = static_cast<uint32_t>(A.n_tests);
@@ -1753,10 +1791,15 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
     const bool leader = lane_ok && tid == 0;
     const uint64_t gi = static_cast<uint64_t>(v) * nt + t;
 
-    // dynamic shared memory: value files | cells | R,W bitsets | per (thread, test)
+    // dynamic shared memory: value files | param table | literal table | cells |
+    // R,W bitsets | per (thread, test)
     const uint32_t warps = blockDim.x >> 5;
     const uint32_t sbase = smem_addr(g_vfs);
-    const uint32_t cell0 = sbase + warps * 32 * A.max_slots * 8;
+    const uint32_t P = static_cast<uint32_t>(A.n_params);
+    const uint32_t lane_slots = kTpTables ? A.lane_slots : A.max_slots;
+    const uint32_t tab0 = sbase + warps * 32 * lane_slots * 8;
+    const uint32_t lit0 = tab0 + Ln * (P + 2) * 8;
+    const uint32_t cell0 = lit0 + A.max_lits * 8;
     const uint32_t smem_cells = kGC ? 0 : A.n_cells;
     const uint32_t back0 = cell0 + Ln * smem_cells * 8; // phase-start copy of the cells
     const uint32_t bits0 = back0 + (A.tp_snap ? Ln * smem_cells * 8 : 0);
@@ -1768,8 +1811,11 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
 
     Lane<kM> L;
     L.gvf = nullptr;
-    L.vsh = sbase + (w * 32 * A.max_slots + l) * 8;
+    L.vsh = sbase + (w * 32 * lane_slots + l) * 8;
     L.vstr = 32 * 8;
+    L.tsh = tab0 + j * 8;
+    L.tstr = Ln * 8;
+    L.lsh = lit0;
     L.base = 0;
     L.row = 0;
     L.v = v;
@@ -1831,7 +1877,9 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
     __syncthreads();
 
     const gevo_variant var = A.variants[v];
-    const uint32_t P = static_cast<uint32_t>(A.n_params);
+    // CTA-shared tables: the variant's literals, each test's parameters
+    for (uint32_t k = threadIdx.x; k < var.n_lits; k += blockDim.x)
+        sts2(lit0 + k * 8, __ldg(A.lit_payload + var.lit_base + k), __ldg(A.lit_tag + var.lit_base + k));
     Thread th{0, 0, -1, 0, 0, false};
     Thread th_snap = th;
     int64_t cost_commit = 0, ir_commit = 0;
@@ -1844,16 +1892,20 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
         L.n_values = var.n_values;
         L.n_slots = var.n_slots;
         L.writable = var.writable;
-        const uint32_t lit_begin = var.n_values + P + 2;
-        L.stage_base = lit_begin + var.n_lits;
-        const size_t tp0 = static_cast<size_t>(t) * P;
-        for (uint32_t p = 0; p < P; ++p)
-            L.W(var.n_values + p, A.param_payload[tp0 + p], A.param_tag[tp0 + p]);
-        L.W(var.n_values + P, 0, GEVO_TAG_POISON_PARAM);
-        L.W(var.n_values + P + 1, 0, GEVO_TAG_POISON_MISSING);
-        for (uint32_t k = 0; k < var.n_lits; ++k)
-            L.W(lit_begin + k, __ldg(A.lit_payload + var.lit_base + k),
-                __ldg(A.lit_tag + var.lit_base + k));
+        L.nv = var.n_values;
+        L.lit_begin = var.n_values + P + 2;
+        L.stage_base = L.lit_begin + var.n_lits;
+        if (!kTpTables)
+            for (uint32_t k = 0; k < var.n_lits; ++k)
+                L.W(L.lit_begin + k, __ldg(A.lit_payload + var.lit_base + k),
+                    __ldg(A.lit_tag + var.lit_base + k));
+        if (tid == 0 || !kTpTables) {
+            const size_t tp0 = static_cast<size_t>(t) * P;
+            for (uint32_t p = 0; p < P; ++p)
+                L.W(var.n_values + p, A.param_payload[tp0 + p], A.param_tag[tp0 + p]);
+            L.W(var.n_values + P, 0, GEVO_TAG_POISON_PARAM);
+            L.W(var.n_values + P + 1, 0, GEVO_TAG_POISON_MISSING);
+        }
         tp_reset_thread(L, th);
         tp_init_cells(A, L, tid, T);
     }
@@ -1882,23 +1934,27 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
         }
         __syncthreads();
         int kind = kStopIdle;
-        if (st == kInstPar) {
-            L.seq = false;
-            kind = run_thread(A, L, th, first_fail);
-            if (kind == kStopTrap)
-                atomicMin(S.min_stop + j, static_cast<int32_t>(tid));
-        }
-        if (__syncthreads_or(st == kInstSeq)) {
-            // reference schedule: thread after thread, stop at the first trap
-            for (uint32_t u = 0; u < T; ++u) {
-                if (u == tid && st == kInstSeq && S.min_stop[j] == INT32_MAX) {
-                    L.seq = true;
-                    kind = run_thread(A, L, th, first_fail);
-                    if (kind == kStopTrap)
+        // round 0 runs the concurrent instances; when some instance follows the
+        // reference schedule, rounds 1..T run its threads one after another,
+        // stopping at the first trap (one run_thread call site: inlined)
+        const bool any_seq = __syncthreads_or(st == kInstSeq);
+        const uint32_t rounds = any_seq ? T + 1 : 1;
+        for (uint32_t u = 0; u < rounds; ++u) {
+            const bool go = u == 0 ? st == kInstPar
+                                   : (st == kInstSeq && tid == u - 1 &&
+                                      S.min_stop[j] == INT32_MAX);
+            if (go) {
+                L.seq = u != 0;
+                kind = run_thread(A, L, th, first_fail);
+                if (kind == kStopTrap) {
+                    if (u == 0)
+                        atomicMin(S.min_stop + j, static_cast<int32_t>(tid));
+                    else
                         S.min_stop[j] = static_cast<int32_t>(tid);
                 }
-                __syncthreads();
             }
+            if (any_seq)
+                __syncthreads();
         }
         if (lane_ok) {
             sts1(pq0 + q * 4, static_cast<uint32_t>(kind));
@@ -2227,17 +2283,19 @@ cudaError_t launch_interp(const InterpArgs& A, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
-size_t tp_smem_bytes(uint32_t threads, uint32_t lanes, uint32_t max_slots, uint32_t n_cells,
+size_t tp_smem_bytes(uint32_t threads, uint32_t lanes, const TpTables& tab, uint32_t n_cells,
                      uint32_t n_chunks, bool backup) {
     const uint32_t K = 32 / lanes;
     const size_t warps = (threads + K - 1) / K;
     const size_t Q = static_cast<size_t>(threads) * lanes;
-    size_t b = warps * 32 * max_slots * 8 + static_cast<size_t>(lanes) * n_cells * 8 * (backup ? 2 : 1) +
+    size_t b = warps * 32 * (kTpTables ? tab.lane_slots : tab.max_slots) * 8 +
+               (static_cast<size_t>(lanes) * (tab.n_params + 2) + tab.max_lits) * 8 +
+               static_cast<size_t>(lanes) * n_cells * 8 * (backup ? 2 : 1) +
                2 * static_cast<size_t>(n_chunks) * warps * 32 * 4 + 4 * Q * 4;
     return ((b + 7) & ~size_t(7)) + Q * 8;
 }
 
-TpShape tp_shape(uint32_t threads, uint32_t n_tests, uint32_t max_slots, uint32_t n_cells,
+TpShape tp_shape(uint32_t threads, uint32_t n_tests, const TpTables& tab, uint32_t n_cells,
                  uint32_t n_chunks, bool backup) {
     TpShape s{0, 0, 0};
     if (threads < 1 || threads > kTpMaxBlock)
@@ -2249,7 +2307,7 @@ TpShape tp_shape(uint32_t threads, uint32_t n_tests, uint32_t max_slots, uint32_
         const uint32_t warps = (threads + K - 1) / K;
         if (warps * 32 > kTpMaxBlock)
             continue;
-        const size_t bytes = tp_smem_bytes(threads, ln, max_slots, n_cells, n_chunks, backup);
+        const size_t bytes = tp_smem_bytes(threads, ln, tab, n_cells, n_chunks, backup);
         if (bytes <= kSmemBudget) {
             s.warps_per_cta = warps;
             s.lanes = ln;
@@ -2265,8 +2323,8 @@ cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream) {
         return cudaSuccess;
     const bool gc = A.gcells != nullptr;
     const TpShape s = tp_shape(static_cast<uint32_t>(A.threads), static_cast<uint32_t>(A.n_tests),
-                               A.max_slots, gc ? 0 : A.n_cells, gc ? 0 : A.n_chunks,
-                               A.tp_snap != nullptr);
+                               TpTables{A.lane_slots, A.max_slots, static_cast<uint32_t>(A.n_params), A.max_lits},
+                               gc ? 0 : A.n_cells, gc ? 0 : A.n_chunks, A.tp_snap != nullptr);
     if (s.warps_per_cta == 0 || s.lanes != A.tp_lanes)
         return cudaErrorInvalidConfiguration;
     const unsigned grid = A.n_var * ((static_cast<uint32_t>(A.n_tests) + s.lanes - 1) / s.lanes);

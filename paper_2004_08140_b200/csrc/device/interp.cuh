@@ -91,6 +91,8 @@ struct InterpArgs {
 
     // thread-parallel lanes (interp_tp_kernel)
     uint32_t tp_lanes;              // tests per CTA (thread-parallel kernel)
+    uint32_t lane_slots;            // per-lane value-file slots: max n_values + max_phis
+    uint32_t max_lits;              // max literals of a variant (CTA-shared table)
     uint2* gcells;                  // [cell][instance] global instance memory (null: on chip)
     unsigned long long* gshadow;    // [cell][instance] same-phase access records
     uint2* out_cells;               // [cell][instance] final memory of completed instances
@@ -116,7 +118,10 @@ constexpr uint32_t kSpinLog = 8;
 constexpr uint32_t kMaxSlots = GEVO_MAX_SLOTS;
 
 // Largest CTA of the thread-parallel interpreter.
-constexpr uint32_t kTpMaxBlock = 512;
+#ifndef GEVO_TP_MAX_BLOCK
+#define GEVO_TP_MAX_BLOCK 512
+#endif
+constexpr uint32_t kTpMaxBlock = GEVO_TP_MAX_BLOCK;
 
 // Shared memory available to the value file of one CTA.
 constexpr size_t kSmemBudget = 200 * 1024;
@@ -143,7 +148,13 @@ struct TpShape {
     uint32_t lanes;         // tests per CTA (<= 32); 32 / lanes simulated threads per warp
     size_t smem;
 };
-TpShape tp_shape(uint32_t threads, uint32_t n_tests, uint32_t max_slots, uint32_t n_cells,
+struct TpTables {
+    uint32_t lane_slots;    // max over variants of n_values + max_phis
+    uint32_t max_slots;     // max over variants of every value-file slot
+    uint32_t n_params;
+    uint32_t max_lits;
+};
+TpShape tp_shape(uint32_t threads, uint32_t n_tests, const TpTables& tab, uint32_t n_cells,
                  uint32_t n_chunks, bool backup);
 cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream);
 cudaError_t launch_error(const uint32_t* cand, const uint32_t* orc, const uint8_t* elem, uint32_t n,

@@ -225,6 +225,8 @@ void bind_batch(gevo::InterpArgs& A, const void* dblob, const gevo_batch_header&
     A.lit_tag = reinterpret_cast<const uint8_t*>(base + h.off_lit_tag);
     A.n_variants = h.n_variants;
     A.max_slots = std::max<uint32_t>(h.max_slots, 1);
+    A.lane_slots = std::max<uint32_t>(h.max_lane_slots, 1);
+    A.max_lits = h.max_lits;
     A.ts_slots = std::max<uint32_t>(h.max_values, 1);
 }
 
@@ -325,10 +327,11 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
     const uint32_t n_chunks = std::max<uint32_t>((n_cells + 31) / 32, 1);
     const uint32_t threads = static_cast<uint32_t>(std::max(ex.threads, 1));
     // on-chip instance memory first; global cells when it does not fit
-    gevo::TpShape tps = gevo::tp_shape(threads, T, A.max_slots, n_cells, n_chunks, h.any_sync != 0);
+    const gevo::TpTables tab{A.lane_slots, A.max_slots, static_cast<uint32_t>(S.n_params), A.max_lits};
+    gevo::TpShape tps = gevo::tp_shape(threads, T, tab, n_cells, n_chunks, h.any_sync != 0);
     bool gc = false;
     if (tps.warps_per_cta == 0) {
-        tps = gevo::tp_shape(threads, T, A.max_slots, 0, 0, false);
+        tps = gevo::tp_shape(threads, T, tab, 0, 0, false);
         gc = tps.warps_per_cta > 0;
     }
     if (ex.threads >= 1 && !opt.sequential && tps.warps_per_cta > 0 && tp_enabled()) {

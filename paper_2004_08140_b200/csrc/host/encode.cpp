@@ -446,6 +446,8 @@ void BatchImage::add(const Kernel& k) {
     slot_value_.push_back(std::move(slot_ids));
     max_slots_ = std::max(max_slots_, var.n_slots);
     max_values_ = std::max<uint32_t>(max_values_, V);
+    max_lits_ = std::max<uint32_t>(max_lits_, var.n_lits);
+    max_lane_slots_ = std::max<uint32_t>(max_lane_slots_, V + var.max_phis);
     any_sync_ = any_sync_ || (var.flags & GEVO_VAR_HAS_SYNC);
     dirty_ = true;
 }
@@ -471,6 +473,8 @@ const std::vector<uint8_t>& BatchImage::blob() {
     h.max_slots = max_slots_;
     h.max_values = max_values_;
     h.any_sync = any_sync_ ? 1 : 0;
+    h.max_lits = max_lits_;
+    h.max_lane_slots = max_lane_slots_;
     uint64_t off = align(sizeof(gevo_batch_header));
     h.off_variants = off;
     off = align(off + variants_.size() * sizeof(gevo_variant));

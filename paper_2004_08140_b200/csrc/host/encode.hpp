@@ -83,6 +83,8 @@ private:
     bool dirty_ = true;
     uint32_t max_slots_ = 0;
     uint32_t max_values_ = 0;
+    uint32_t max_lits_ = 0;
+    uint32_t max_lane_slots_ = 0;
     bool any_sync_ = false;
 };
 
