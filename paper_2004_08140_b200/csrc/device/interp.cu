@@ -1257,11 +1257,19 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
     // fell-off sentinel record, and the batch array is padded, so the
     // one-ahead prefetch never leaves it.
     uint32_t pc = b.start + static_cast<uint32_t>(th.ip);
+#ifdef GEVO_PREFETCH
     uint4 nxt = __ldg(code + pc);
+#endif
     for (;;) {
+#ifdef GEVO_PREFETCH
         const uint4 r = nxt;
         nxt = __ldg(code + pc + 1);
-        const uint32_t op = f_op(r);
+#else
+        // (a one-ahead prefetch measured slower: the loop-carried copy of the
+        // prefetched record waits for the load anyway)
+        uint4 r = __ldg(code + pc);
+#endif
+        uint32_t op = f_op(r);
         if (th.slow || S.mode == 2) {
             // exact per-instruction charging near the budget / abstract iterate
             if (op != GEVO_OP_PHI && op != GEVO_OP_FELL) {
@@ -1273,6 +1281,46 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
                     spin_abandon(S, th, L, 0x80 | op);
             }
         }
+#ifndef GEVO_NO_ARITH_RUN
+        else if (op <= GEVO_OP_FCMP && op != GEVO_OP_SDIV && op != GEVO_OP_FDIV) {
+            // Straight-line run of plain arithmetic (block-level charging, no
+            // abstract iterate): a tight loop in which only pc and the record
+            // are live. It stops at the first instruction it does not handle
+            // (another opcode, a division, a tag mismatch, a missing result
+            // slot), which the general dispatch below then executes.
+            for (;;) {
+                const uint2 x = L.V(f_a(r)), y = L.V(f_b(r));
+                const uint32_t otag = f_otag(r);
+                const uint32_t res = f_res(r);
+                if (x.y != otag || y.y != otag || res == GEVO_NO_RESULT)
+                    break;
+                const float fx = __uint_as_float(x.x), fy = __uint_as_float(y.x);
+                uint32_t v, vt = otag;
+                switch (op) {
+                case GEVO_OP_ADD: v = x.x + y.x; break;
+                case GEVO_OP_SUB: v = x.x - y.x; break;
+                case GEVO_OP_MUL: v = x.x * y.x; break;
+                case GEVO_OP_FADD: v = __float_as_uint(__fadd_rn(fx, fy)); break;
+                case GEVO_OP_FSUB: v = __float_as_uint(__fsub_rn(fx, fy)); break;
+                case GEVO_OP_FMUL: v = __float_as_uint(__fmul_rn(fx, fy)); break;
+                case GEVO_OP_ICMP:
+                    v = cmp(static_cast<int32_t>(x.x), static_cast<int32_t>(y.x), f_aux(r)) ? 1u : 0u;
+                    vt = GEVO_TAG_BOOL;
+                    break;
+                default: // FCMP
+                    v = cmp(fx, fy, f_aux(r)) ? 1u : 0u;
+                    vt = GEVO_TAG_BOOL;
+                    break;
+                }
+                L.W(res, v, vt);
+                ++pc;
+                r = __ldg(code + pc);
+                op = f_op(r);
+                if (op > GEVO_OP_FCMP || op == GEVO_OP_SDIV || op == GEVO_OP_FDIV)
+                    break;
+            }
+        }
+#endif
         bool ok;
         if (op <= GEVO_OP_FCMP) {
             // i32 / f32 arithmetic and compares: both operands carry otag
@@ -1401,7 +1449,9 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
             if ((th.executed >= S.next || S.mode != 0) && !th.slow)
                 spin_at_entry(A, L, th, S);
             pc = b.start + static_cast<uint32_t>(th.ip);
+#ifdef GEVO_PREFETCH
             nxt = __ldg(code + pc);
+#endif
             continue;
         } else if (op == GEVO_OP_LOAD || op == GEVO_OP_STORE) {
             ok = mem_op(A, L, r);
