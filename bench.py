@@ -208,11 +208,19 @@ def b200_arm(args):
     from paper_2004_08140_b200 import dist as gdist
 
     rank, local, world = dist_env()
+    # one process per GPU; more ranks than GPUs (a functional check of the
+    # N > 1 path on a smaller box) share devices round-robin
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     os.environ["GEVO_DEVICE"] = str(local)
+    coll_dev = "cuda" if os.environ.get("BENCH_DIST_BACKEND", "nccl") == "nccl" else "cpu"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     stream = torch.cuda.current_stream()
     gevo.set_stream(stream.cuda_stream)
 
@@ -250,7 +258,7 @@ def b200_arm(args):
         # then the GPU non-dominated sort of the gathered population.
         nonlocal gathered_front
         rows = gdist.fitness_rows(np.concatenate(vrec_list))
-        g = gdist.allgather_fitness(rows, device="cuda") if world > 1 else rows
+        g = gdist.allgather_fitness(rows, device=coll_dev) if world > 1 else rows
         cost, err, _ = gdist.accepted_fitness(g)
         front, _, _ = gevo.rank(cost, err)
         gathered_front = front
@@ -315,7 +323,7 @@ def b200_arm(args):
 
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms, e2e_ms = t.tolist()
 

@@ -16,6 +16,10 @@
 //                              tournament_select
 //   run <bench> <seed> <pop> <gens> <mode> <train> <heldout> <outdir>
 //                              reference CLI run (log.csv, report.json)
+//   authored <kernel.ir> <gen.json> <n_tests> <seed> <patches.txt> <budget> <tol>
+//                              an authored kernel (configs 3-4): generate_tests_for,
+//                              then per patch (line 0 = original) per-test execute
+//                              records and the EvalOutcome
 
 #include "evoir/cli_app.hpp"
 #include "evoir/corpus.hpp"
@@ -26,6 +30,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <iostream>
 #include <sstream>
 
@@ -459,6 +464,51 @@ int cmd_run(int argc, char** argv) {
     return cli::cmd_run(opt);
 }
 
+std::string slurp(const std::string& path) {
+    std::ifstream f(path);
+    std::stringstream ss;
+    ss << f.rdbuf();
+    return ss.str();
+}
+
+int cmd_authored(int argc, char** argv) {
+    if (argc < 9) {
+        std::cerr << "usage: ref_dump authored <ir> <gen.json> <n_tests> <seed> <patches> <budget> <tol>\n";
+        return 1;
+    }
+    const Kernel k = parse_kernel(slurp(argv[2]));
+    const GeneratorSpec gen = generator_spec_from_json(slurp(argv[3]));
+    const int n_tests = std::stoi(argv[4]);
+    const uint64_t seed = std::stoull(argv[5]);
+    const double tol = std::stod(argv[8]);
+    auto tests = generate_tests_for(k, gen, n_tests, seed);
+    ExecConfig cfg = ExecConfig::for_kernel(k);
+    cfg.instruction_budget = std::stoll(argv[7]);
+    std::ifstream in(argv[6]);
+    std::string line;
+    int i = 0;
+    while (std::getline(in, line)) {
+        if (line.empty())
+            continue;
+        json j;
+        j["kind"] = "authored";
+        j["i"] = i++;
+        j["patch"] = json::parse(line);
+        const Kernel v = apply_patch(k, patch_from_json(line)).kernel;
+        j["valid"] = is_valid(v);
+        json per = json::array();
+        for (const auto& t : tests)
+            per.push_back(exec_json(v, t, cfg));
+        j["tests"] = per;
+        const EvalOutcome o = evaluate_fitness(v, tests, cfg, tol);
+        j["outcome"] = {{"accepted", o.accepted}, {"failing_test", o.failing_test},
+                        {"reason", o.reason}, {"cost", hexd(o.fitness.cost)},
+                        {"error", hexd(o.fitness.error)}};
+        std::cout << j.dump() << "\n";
+    }
+    return 0;
+}
+
 } // namespace
 
 int main(int argc, char** argv) {
@@ -478,6 +528,8 @@ int main(int argc, char** argv) {
         return cmd_nsga(argc > 2 ? std::stoi(argv[2]) : 200);
     if (cmd == "run")
         return cmd_run(argc, argv);
+    if (cmd == "authored")
+        return cmd_authored(argc, argv);
     std::cerr << "unknown subcommand\n";
     return 1;
 }

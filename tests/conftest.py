@@ -49,3 +49,10 @@ def gevo():
     import paper_2004_08140_b200 as g
     g.lib()
     return g
+
+
+def authored_fixture(name):
+    """(suite header, records) of tests/golden/authored_<name>.jsonl.gz
+    (oracle/gen_golden_authored.py, compiled reference)."""
+    rows = load_jsonl("authored_%s.jsonl.gz" % name)
+    return rows[0], rows[1:]

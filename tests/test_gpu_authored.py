@@ -98,3 +98,33 @@ def test_authored_original_large(gevo, name, scale):
     assert exp["status"] == "completed" and int(got["status"]) == 0
     assert int(got["cost"]) == exp["cost"] and int(got["ir"]) == exp["ir"]
     assert float(got["error"]) == 0.0 == exp["error"]
+
+
+@pytest.mark.parametrize("name", ["svm-rbf", "conv-bn"])
+def test_authored_golden_records(gevo, name):
+    """Device records and verdicts against the compiled reference's fixture
+    (oracle/gen_golden_authored.py)."""
+    from conftest import authored_fixture
+    head, recs = authored_fixture(name)
+    ir, _ = gevo.authored_kernel(name)
+    suite = gevo.Suite.from_spec(ir, json.dumps(head["gen"]), head["n_tests"], head["seed"])
+    cfg = suite.exec_config().with_(budget=head["budget"])
+    batch = suite.batch()
+    for rec in recs:
+        batch.add_patch(json.dumps(rec["patch"]))
+    vr, tr, _ = batch.eval(cfg, tolerance=head["tol"], tests=True)
+    for v, rec in enumerate(recs):
+        for t, exp in enumerate(rec["tests"]):
+            got = tr[v, t]
+            where = (name, rec["i"], t)
+            assert STATUS[int(got["status"])] == exp["status"], where
+            assert int(got["cost"]) == exp["cost"] and int(got["ir"]) == exp["ir"], where
+            if exp["status"] == "completed":
+                assert hex_double(float(got["error"])) == exp["err"], where
+            else:
+                assert batch.reason(v, int(got["code"]), int(got["aux"])) == exp["reason"], where
+        assert bool(vr[v]["accepted"]) == rec["outcome"]["accepted"], (name, rec["i"])
+        assert int(vr[v]["failing_test"]) == rec["outcome"]["failing_test"], (name, rec["i"])
+        if rec["outcome"]["accepted"]:
+            assert hex_double(float(vr[v]["cost_mean"])) == rec["outcome"]["cost"]
+            assert hex_double(float(vr[v]["error_max"])) == rec["outcome"]["error"]

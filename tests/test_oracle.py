@@ -106,3 +106,32 @@ def test_oracle_nsga(nsga_golden):
         assert fronts == case["fronts"]
         assert [hex_double(float(x)) for x in crowd] == case["crowding"]
         assert ob.select_best(cost, err, case["keep"]) == case["select_best"]
+
+
+@pytest.mark.parametrize("name", ["svm-rbf", "conv-bn"])
+def test_oracle_authored_kernels(gevo, name):
+    """Authored config-3/4 kernels (reduced sizes): the oracle reproduces the
+    compiled reference's per-test records for the original and 40 mutants."""
+    from conftest import authored_fixture
+    head, recs = authored_fixture(name)
+    ir, _ = gevo.authored_kernel(name)
+    gen = json.dumps(head["gen"])
+    docs = gevo.spec_inputs(gen, head["n_tests"], head["seed"])
+    k0 = ob.Kernel(ir)
+    cfg = _cfg_for(ir, head["budget"])
+    tests = []
+    for d in docs:
+        doc = {"inputs": d["inputs"], "scalars": d.get("scalars", {}), "oracle": {}}
+        res = ob.execute(k0, ob.CTest(doc), cfg)
+        doc["oracle"] = res["outputs"]
+        tests.append(ob.CTest(doc))
+    for rec in recs:
+        k = ob.Kernel(gevo.apply_patch(ir, json.dumps(rec["patch"]))[0])
+        for t, exp in zip(tests, rec["tests"]):
+            r = ob.execute(k, t, cfg)
+            where = (name, rec["i"])
+            assert (r["status"], r["reason"], r["cost"], r["ir"]) == (
+                exp["status"], exp["reason"], exp["cost"], exp["ir"]), where
+            if exp["status"] == "completed":
+                assert hex_double(r["error"]) == exp["err"], where
+                assert outputs_hash(r["outputs"]) == exp["out"], where
