@@ -45,6 +45,9 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace gevo {
 
 extern __shared__ __align__(16) uint2 g_vfs[]; // value files of the CTA's warps
@@ -2352,7 +2355,11 @@ TpShape tp_shape(uint32_t threads, uint32_t n_tests, const TpTables& tab, uint32
         return s;
     // most tests per CTA first (fuller, converged warps), fewer when the
     // block or its on-chip state would not fit
-    for (uint32_t ln = min(max(n_tests, 1u), 32u); ln >= 1; --ln) {
+    static const uint32_t cap = [] {
+        const char* e = std::getenv("GEVO_TP_LANES"); // tests per CTA upper bound (tuning)
+        return e ? static_cast<uint32_t>(std::max(1, std::min(32, std::atoi(e)))) : 32u;
+    }();
+    for (uint32_t ln = min(max(n_tests, 1u), cap); ln >= 1; --ln) {
         const uint32_t K = 32 / ln;
         const uint32_t warps = (threads + K - 1) / K;
         if (warps * 32 > kTpMaxBlock)
