@@ -109,8 +109,10 @@ __device__ __forceinline__ double word_to_double(uint32_t w, uint32_t elem) {
                                 : static_cast<double>(__uint_as_float(w));
 }
 
+// Undefined / poisoned slot: every tag a slot can hold is 0 (undef), 1..4
+// (i32 f32 bool ptr<shared>), 0x20 / 0x21 (poison) or 0x40 | param (ptr<global>).
 __device__ __forceinline__ bool bad_tag(uint32_t t) {
-    return t == GEVO_TAG_UNDEF || t == GEVO_TAG_POISON_PARAM || t == GEVO_TAG_POISON_MISSING;
+    return (t - 1u > 3u) && (t < static_cast<uint32_t>(GEVO_TAG_PTR_GLOBAL));
 }
 
 // Branch-free select (the compiler may not re-branch an asm selp).
@@ -189,6 +191,7 @@ struct Lane {
     uint32_t row;
     // program
     const gevo_inst* code;
+    const int64_t* suffix; // per-instruction cost of the rest of its block (this launch)
     const uint4* dblk;  // block records of this variant
     const gevo_arm* arm;
     uint32_t n_values;
@@ -371,6 +374,8 @@ __device__ __noinline__ int64_t suffix_cost_of(const int64_t* cost, const gevo_i
 template <int kM>
 __device__ __forceinline__ int64_t suffix_cost(const InterpArgs& A, const Lane<kM>& L, const Blk& b,
                                                uint32_t from) {
+    if (L.suffix) // per-launch table: cost of [ip, len) for every instruction
+        return from < b.len ? __ldg(L.suffix + b.start + from) : 0;
     return suffix_cost_of(A.cost, L.code, b.start, b.len, from);
 }
 
@@ -1677,6 +1682,7 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
         const gevo_variant var = A.variants[v];
         const uint32_t P = static_cast<uint32_t>(A.n_params);
         L.code = A.insts + var.inst_base;
+        L.suffix = A.suffix ? A.suffix + var.inst_base : nullptr;
         L.dblk = A.dblocks + var.block_base;
         L.arm = A.arms + var.arm_base;
         L.n_values = var.n_values;
@@ -1940,6 +1946,7 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
     const bool snap = A.tp_snap && (var.flags & GEVO_VAR_HAS_SYNC);
     if (active && S.state[j] != kInstDone) {
         L.code = A.insts + var.inst_base;
+        L.suffix = A.suffix ? A.suffix + var.inst_base : nullptr;
         L.dblk = A.dblocks + var.block_base;
         L.arm = A.arms + var.arm_base;
         L.n_values = var.n_values;
@@ -2197,7 +2204,8 @@ struct CostTableArg {
 __global__ void block_cost_kernel(const gevo_variant* __restrict__ variants,
                                   const gevo_block* __restrict__ blocks,
                                   const gevo_inst* __restrict__ insts, uint32_t n_variants,
-                                  const CostTableArg ct, uint4* __restrict__ out) {
+                                  const CostTableArg ct, uint4* __restrict__ out,
+                                  int64_t* __restrict__ suffix) {
     const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n_variants)
         return;
@@ -2205,8 +2213,11 @@ __global__ void block_cost_kernel(const gevo_variant* __restrict__ variants,
     for (uint32_t b = 0; b < var.n_blocks; ++b) {
         const gevo_block g = blocks[var.block_base + b];
         int64_t c = 0;
-        for (uint32_t j = 0; j < g.len; ++j)
+        for (uint32_t j = g.len; j-- > 0;) {
             c += ct.c[insts[var.inst_base + g.start + j].cls];
+            if (suffix)
+                suffix[var.inst_base + g.start + j] = c;
+        }
         const uint64_t u = static_cast<uint64_t>(c);
         out[var.block_base + b] =
             make_uint4(g.start, static_cast<uint32_t>(g.len) | (static_cast<uint32_t>(g.nphi) << 16),
@@ -2307,14 +2318,15 @@ LaunchShape interp_shape(int32_t n_tests, uint32_t max_slots) {
 
 cudaError_t launch_block_cost(const gevo_block* blocks, const gevo_inst* insts,
                               const gevo_variant* variants, uint32_t n_variants,
-                              const int64_t* cost_table, uint4* out, cudaStream_t stream) {
+                              const int64_t* cost_table, uint4* out, int64_t* suffix,
+                              cudaStream_t stream) {
     if (n_variants == 0)
         return cudaSuccess;
     CostTableArg ct;
     for (int i = 0; i < GEVO_COST_CLASSES; ++i)
         ct.c[i] = cost_table[i];
     block_cost_kernel<<<(n_variants + 127) / 128, 128, 0, stream>>>(variants, blocks, insts,
-                                                                    n_variants, ct, out);
+                                                                    n_variants, ct, out, suffix);
     return cudaGetLastError();
 }
 

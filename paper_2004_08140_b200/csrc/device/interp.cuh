@@ -26,6 +26,7 @@ struct InterpArgs {
     const uint32_t* lit_payload;
     const uint8_t* lit_tag;
     const uint4* dblocks;          // [batch block] {start, len | nphi << 16, cost (int64)}
+    const int64_t* suffix;         // [batch instruction] cost of the rest of its block
     uint32_t n_variants;
 
     // suite
@@ -138,7 +139,8 @@ LaunchShape interp_shape(int32_t n_tests, uint32_t max_slots);
 // cost table) that the interpreter reads with one 16-byte load per block entry.
 cudaError_t launch_block_cost(const gevo_block* blocks, const gevo_inst* insts,
                               const gevo_variant* variants, uint32_t n_variants,
-                              const int64_t* cost_table, uint4* out, cudaStream_t stream);
+                              const int64_t* cost_table, uint4* out, int64_t* suffix,
+                              cudaStream_t stream);
 cudaError_t launch_interp(const InterpArgs& A, cudaStream_t stream);
 
 // Thread-parallel launch shape: warps per CTA and dynamic shared memory, or

@@ -72,7 +72,7 @@ struct DeviceImpl {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     DevBuf blob, rec, vrec, first_fail, priv, sh_tag, sh_val;
     DevBuf ts_pos, ts_prev, ts_exec, ts_stop, ts_val, ts_tag;
-    DevBuf tp_snap, gcells, gshadow, outcells;
+    DevBuf tp_snap, gcells, gshadow, outcells, suffix;
     DevBuf bcost, vf, sp_base, sp_btag, sp_delta, sp_cur, sp_hvary, sp_cvary, sp_log, sp_ld,
         counters;
     DevBuf rank;
@@ -303,11 +303,13 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
 
     // Block costs under this launch's cost table.
     dev.bcost.reserve(std::max<size_t>(h.n_blocks * sizeof(uint4), 16));
+    dev.suffix.reserve(std::max<size_t>(h.n_insts * sizeof(int64_t), 16));
     check(gevo::launch_block_cost(A.blocks, A.insts, A.variants, h.n_variants, ex.cost.data(),
-                                  dev.bcost.as<uint4>(), s),
+                                  dev.bcost.as<uint4>(), dev.suffix.as<int64_t>(), s),
           "block_cost_kernel launch");
     ++launches;
     A.dblocks = dev.bcost.as<uint4>();
+    A.suffix = dev.suffix.as<int64_t>();
 
     const int64_t thr = spin_threshold();
     if (!dev.counters.ptr) {
