@@ -365,12 +365,28 @@ def b200_arm(args):
                                  "lanes_per_warp_inst": (prof[k]["thread_inst"] /
                                                          prof[k]["warp_inst"])
                                  if prof[k].get("thread_inst") else None}
+    # Secondary (HBM) view: DRAM bytes the interpreter launches move (ncu, per
+    # launch) over their live time, against the measured copy bandwidth. The
+    # per-test working sets (<= ~5 KB) stay in L2 / shared memory, so this is
+    # tiny by construction -- the interpreter is not memory-bound.
+    hbm_view = None
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        hbm_peak, hbm_src = peaks["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        hbm_peak, hbm_src = 7700.0, "B200_PROFILING.md fallback"
+    if per_kernel and os.path.exists(ISSUE_PROFILE):
+        prof = json.load(open(ISSUE_PROFILE))["kernels"]
+        dram = sum(prof[k].get("dram_bytes") or 0 for k in KERNELS if k in prof)
+        live_ms = sum(statistics.mean(kernel_ms[k]) for k in KERNELS)
+        gbs = dram / (live_ms / 1e3) / 1e9 if live_ms else 0.0
+        hbm_view = {"achieved_gbs": gbs, "peak_gbs": hbm_peak, "frac": gbs / hbm_peak,
+                    "peak_source": hbm_src}
     roofline = {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "traffic_unit": "DRAM bytes per hot-branch launch (ncu)",
                 "per_kernel": per_kernel,
-                "hbm_note": "algorithmic bytes per execution <= ~5 KB, L2/SMEM resident; "
-                            "HBM (MEASURED_PEAKS hbm_gbs) is not the bound",
+                "hbm_view": hbm_view,
                 "note": "peak = 148 SM x 4 schedulers x 1 warp-inst/cycle x median SM clock"}
 
     cpu = None

@@ -359,6 +359,7 @@ struct Spin {
     uint32_t nst, nld; // store / load log entries of the abstract iterate
     uint32_t retries;  // abstract iterates re-run with a widened hypothesis
     int32_t avoid;     // block not to take as the next anchor (-1: none)
+    uint32_t nvk;      // memory words whose loads are varying (sp_vk)
 };
 
 // Cost of instructions [from, len) of a block (scalar arguments only: a
@@ -673,7 +674,10 @@ __device__ __forceinline__ bool spin_track(const InterpArgs& A, const Lane<kM>& 
             if (A.sp_log[log_at(A, L, j, 0)] == key)
                 hit = j;
         if (op == GEVO_OP_LOAD) {
-            if (hit < kSpinLog && (A.sp_log[log_at(A, L, hit, 2)] & 0x100)) {
+            bool vk = false;
+            for (uint32_t k = 0; k < S.nvk; ++k)
+                vk |= A.sp_vk[static_cast<size_t>(k) * A.n_spin + L.sl] == key;
+            if (vk || (hit < kSpinLog && (A.sp_log[log_at(A, L, hit, 2)] & 0x100))) {
                 vout = 1;
             } else {
                 if (S.nld >= kSpinLog)
@@ -708,6 +712,36 @@ __device__ __forceinline__ bool spin_track(const InterpArgs& A, const Lane<kM>& 
     if (res != GEVO_NO_RESULT)
         spin_set(A, L, res, vout ? 0u : out, vout);
     return true;
+}
+
+// Runs the abstract iterate again from the current anchor entry (S2 becomes
+// the new S1) with the widened hypothesis: varying slots (sp_hvary) and
+// varying memory words (sp_vk) stay varying.
+template <int kM>
+__device__ __forceinline__ void spin_restart_iterate(const InterpArgs& A, Lane<kM>& L, Thread& th,
+                                                     Spin& S) {
+    for (uint32_t x = 0; x < L.n_values; ++x) {
+        const size_t at = sp_at(A, L, x);
+        const uint32_t vary = A.sp_hvary[at];
+        const uint32_t d = vary ? 0u : A.sp_delta[at];
+        A.sp_delta[at] = d;
+        A.sp_base[at] = L.V(x).x;
+        A.sp_cur[at] = d;
+        A.sp_cvary[at] = static_cast<uint8_t>(vary);
+    }
+    for (uint32_t x = L.n_values; x < L.n_slots; ++x) {
+        A.sp_cur[sp_at(A, L, x)] = 0;
+        A.sp_cvary[sp_at(A, L, x)] = 0;
+    }
+    S.e0 = th.executed;
+    S.c0 = L.cost;
+    S.nst = 0;
+    S.nld = 0;
+    S.H = (A.budget - th.executed) / S.p;
+    S.K = S.H;
+    S.Koob = S.H;
+    if (S.H < 3)
+        spin_abandon(S, th, L, 4);
 }
 
 // Protocol step at every completed block entry (phis done).
@@ -773,6 +807,7 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
         S.nst = 0;
         S.nld = 0;
         S.retries = 0;
+        S.nvk = 0;
         S.H = (A.budget - th.executed) / p;
         S.K = S.H;
         S.Koob = S.H;
@@ -810,28 +845,7 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
             spin_abandon(S, th, L, 9);
             return;
         }
-        for (uint32_t x = 0; x < L.n_values; ++x) {
-            const size_t at = sp_at(A, L, x);
-            const uint32_t vary = A.sp_hvary[at];
-            const uint32_t d = vary ? 0u : A.sp_delta[at];
-            A.sp_delta[at] = d;
-            A.sp_base[at] = L.V(x).x;
-            A.sp_cur[at] = d;
-            A.sp_cvary[at] = static_cast<uint8_t>(vary);
-        }
-        for (uint32_t x = L.n_values; x < L.n_slots; ++x) {
-            A.sp_cur[sp_at(A, L, x)] = 0;
-            A.sp_cvary[sp_at(A, L, x)] = 0;
-        }
-        S.e0 = th.executed;
-        S.c0 = L.cost;
-        S.nst = 0;
-        S.nld = 0;
-        S.H = (A.budget - th.executed) / S.p;
-        S.K = S.H;
-        S.Koob = S.H;
-        if (S.H < 3)
-            spin_abandon(S, th, L, 4);
+        spin_restart_iterate(A, L, th, S);
         return;
     }
     // memory: a word the iterate stores a fixed value to and also reads must
@@ -850,13 +864,17 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
             loaded |= A.sp_ld[log_at(A, L, k, 0)] == key;
         if (!loaded)
             continue;
-        if (tf & 0x100) {
-            spin_abandon(S, th, L, 7);
-            return;
-        }
-        if (A.sp_log[log_at(A, L, j, 3)] != A.sp_log[log_at(A, L, j, 1)] ||
+        if ((tf & 0x100) || A.sp_log[log_at(A, L, j, 3)] != A.sp_log[log_at(A, L, j, 1)] ||
             A.sp_log[log_at(A, L, j, 4)] != (tf & 0xFF)) {
-            spin_abandon(S, th, L, 8);
+            // The word a load reads changes from one iteration to the next:
+            // treat its loads as varying (path-irrelevant data) and run the
+            // abstract iterate again; the path obligations then decide.
+            if (S.nvk >= kSpinLog || ++S.retries > 4) {
+                spin_abandon(S, th, L, (tf & 0x100) ? 7 : 8);
+                return;
+            }
+            A.sp_vk[static_cast<size_t>(S.nvk++) * A.n_spin + L.sl] = key;
+            spin_restart_iterate(A, L, th, S);
             return;
         }
     }

@@ -87,6 +87,7 @@ struct InterpArgs {
     uint32_t* sp_log;               // [kSpinLog][col] x 5: store-log key, old payload,
                                     // old tag | flags, last stored payload, last stored tag
     uint32_t* sp_ld;                // [kSpinLog][inst] load-log keys
+    uint32_t* sp_vk;                // [kSpinLog][col] memory words loaded as varying
     int64_t spin_threshold;         // per-thread executed count that arms it
     uint32_t n_spin;                // spin scratch columns (instances, or lanes for tp)
 

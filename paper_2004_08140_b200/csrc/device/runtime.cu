@@ -72,7 +72,7 @@ struct DeviceImpl {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     DevBuf blob, rec, vrec, first_fail, priv, sh_tag, sh_val;
     DevBuf ts_pos, ts_prev, ts_exec, ts_stop, ts_val, ts_tag;
-    DevBuf tp_snap, gcells, gshadow, outcells, suffix;
+    DevBuf tp_snap, gcells, gshadow, outcells, suffix, sp_vk;
     DevBuf bcost, vf, sp_base, sp_btag, sp_delta, sp_cur, sp_hvary, sp_cvary, sp_log, sp_ld,
         counters;
     DevBuf rank;
@@ -179,7 +179,7 @@ size_t scratch_per_instance(const SuiteImage& S, uint64_t writable_any, const Ex
     b += 5 * static_cast<size_t>(std::max(ex.shared_words, 0));
     if (any_sync)
         b += static_cast<size_t>(ex.threads) * (4 + 4 + 8 + 4 + 5 * static_cast<size_t>(max_values));
-    b += 15 * static_cast<size_t>(max_slots) + 24 * gevo::kSpinLog; // spin accelerator
+    b += 15 * static_cast<size_t>(max_slots) + 28 * gevo::kSpinLog; // spin accelerator
     if (vf_global)
         b += 8 * static_cast<size_t>(max_slots);
     return b;
@@ -260,6 +260,8 @@ void reserve_spin(DeviceImpl& dev, gevo::InterpArgs& A, size_t cols) {
     dev.sp_cvary.reserve(n);
     dev.sp_log.reserve(cols * gevo::kSpinLog * 5 * 4);
     dev.sp_ld.reserve(cols * gevo::kSpinLog * 4);
+    dev.sp_vk.reserve(cols * gevo::kSpinLog * 4);
+    A.sp_vk = dev.sp_vk.as<uint32_t>();
     A.sp_hvary = dev.sp_hvary.as<uint8_t>();
     A.sp_cvary = dev.sp_cvary.as<uint8_t>();
     A.sp_log = dev.sp_log.as<uint32_t>();
@@ -341,7 +343,7 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
         const uint32_t tgroups = (T + tps.lanes - 1) / tps.lanes;
         A.n_cells = n_cells;
         A.n_chunks = n_chunks;
-        const size_t per_lane = thr > 0 ? 15 * static_cast<size_t>(A.max_slots) + 24 * gevo::kSpinLog
+        const size_t per_lane = thr > 0 ? 15 * static_cast<size_t>(A.max_slots) + 28 * gevo::kSpinLog
                                         : 0;
         const size_t lanes_per_variant = static_cast<size_t>(tgroups) * 32 * tps.warps_per_cta;
         // global cells + access records: 16 bytes per cell per instance

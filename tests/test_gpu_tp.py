@@ -148,6 +148,25 @@ done:
   store out[%0], %5  #uid=10
   ret  #uid=11
 }""",
+    # thread 0 spins reading and rewriting a word whose value changes every
+    # iteration (path-irrelevant): the accelerator treats the load as varying
+    "varying_word_spin": """kernel k(out: ptr<global> f32, s: ptr<shared> f32) threads=8 shared=8 {
+entry:
+  %0 = tid i32  #uid=0
+  store s[%0], 1.0  #uid=1
+  br loop  #uid=2
+loop:
+  %1 = phi i32 [0, entry], [%5, loop]  #uid=3
+  %2 = load f32 s[%0]  #uid=4
+  %3 = fadd f32 %2, 1.0  #uid=5
+  store s[%0], %3  #uid=6
+  %5 = add i32 %1, %0  #uid=7
+  %6 = icmp.lt i32 %5, 50  #uid=8
+  br %6, loop, done  #uid=9
+done:
+  store out[%0], %3  #uid=10
+  ret  #uid=11
+}""",
 }
 
 
