@@ -138,6 +138,20 @@ typedef struct {
     uint16_t ref;       /* operand ref */
 } gevo_arm;
 
+/* Per-instruction edge record (parallel to the instruction array; used for br):
+ * the leading phis of each target block resolved for this branch's block as
+ * the predecessor (src/vm.cpp:311-323 picks the first arm whose label is the
+ * predecessor). phi[e][j] = operand ref | result slot << 16 for edge e (0 =
+ * first target, 1 = second) and phi j < 2; ref GEVO_EDGE_NOINC = no matching
+ * arm. GEVO_EDGE_NONE in phi[e][0] = not pre-resolved (> 2 phis, a phi without
+ * result id, unknown target): the interpreter matches arms itself. */
+typedef struct {
+    uint32_t phi[2][2];
+} gevo_edge;
+
+#define GEVO_EDGE_NOINC 0xFFFEu
+#define GEVO_EDGE_NONE 0xFFFFFFFFu
+
 typedef struct {
     uint32_t start;  /* instruction index relative to the variant's inst base */
     uint16_t len;
@@ -177,11 +191,12 @@ typedef struct {
     uint32_t pad;
     /* byte offsets of each section from the start of the blob */
     uint64_t off_variants, off_blocks, off_insts, off_arms, off_lit_payload, off_lit_tag;
+    uint64_t off_edges;
     uint64_t total_bytes;
 } gevo_batch_header;
 
 #define GEVO_MAGIC 0x4F564547u
-#define GEVO_VERSION 4u
+#define GEVO_VERSION 5u
 
 /* Per-(variant, test) record written by the interpreter. */
 typedef struct {

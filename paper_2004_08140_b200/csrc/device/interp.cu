@@ -192,6 +192,7 @@ struct Lane {
     // program
     const gevo_inst* code;
     const int64_t* suffix; // per-instruction cost of the rest of its block (this launch)
+    const gevo_edge* edges; // per-instruction pre-resolved branch phis
     const uint4* dblk;  // block records of this variant
     const gevo_arm* arm;
     uint32_t n_values;
@@ -963,7 +964,7 @@ __device__ __forceinline__ bool phi_arm(const Lane<kM>& L, const uint4 r, int32_
 // enter_block (vm.cpp:293-333): charge and stage every leading phi, then write.
 template <int kM>
 __device__ __forceinline__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Thread& th,
-                            int32_t target, Blk& b, Spin& S) {
+                            int32_t target, Blk& b, Spin& S, uint2 edge) {
     th.prev = th.block;
     th.block = target;
     th.ip = 0;
@@ -974,6 +975,35 @@ __device__ __forceinline__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Th
     if (n == 0)
         return true;
     const bool track = S.mode == 2;
+    if (!th.slow && !track && edge.x != GEVO_EDGE_NONE) {
+        // <= 2 phis resolved for this edge at encode time (no arm matching)
+        const uint32_t ref0 = edge.x & 0xFFFF;
+        uint2 v0, v1;
+        if (ref0 == GEVO_EDGE_NOINC) {
+            refund(A, L, th, b, 1);
+            return L.trap(GEVO_TRAP_PHI_NO_INCOMING);
+        }
+        if (!L.fetch(ref0, v0)) {
+            refund(A, L, th, b, 1);
+            return false;
+        }
+        th.ip = 1;
+        if (n == 2) {
+            const uint32_t ref1 = edge.y & 0xFFFF;
+            if (ref1 == GEVO_EDGE_NOINC) {
+                refund(A, L, th, b, 2);
+                return L.trap(GEVO_TRAP_PHI_NO_INCOMING);
+            }
+            if (!L.fetch(ref1, v1)) {
+                refund(A, L, th, b, 2);
+                return false;
+            }
+            th.ip = 2;
+            L.W(edge.y >> 16, v1.x, v1.y);
+        }
+        L.W(edge.x >> 16, v0.x, v0.y);
+        return true;
+    }
     if (n == 2 && !th.slow && !track) {
         // loop headers: both arms read before either phi writes (parallel copy)
         const uint4 r0 = fetch_inst(L.code, b.start), r1 = fetch_inst(L.code, b.start + 1);
@@ -1437,6 +1467,7 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
         } else if (op == GEVO_OP_BR) {
             th.ip = static_cast<int32_t>(pc - b.start);
             int32_t target = f_t0(r);
+            bool second = false;
             if (f_aux(r) == 2) {
                 const uint2 c = L.V(f_a(r));
                 if (c.y != GEVO_TAG_BOOL) {
@@ -1444,7 +1475,8 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
                     refund(A, L, th, b, th.ip + 1);
                     return kStopTrap;
                 }
-                target = c.x ? f_t0(r) : f_t1(r);
+                second = c.x == 0;
+                target = second ? f_t1(r) : f_t0(r);
             }
             refund(A, L, th, b, th.ip + 1);
             if (target < 0) {
@@ -1470,7 +1502,9 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
                     return kStopTrap;
                 }
             }
-            if (!enter_block(A, L, th, target, b, S))
+            const uint4 er = __ldg(reinterpret_cast<const uint4*>(L.edges + pc));
+            if (!enter_block(A, L, th, target, b, S,
+                             second ? make_uint2(er.z, er.w) : make_uint2(er.x, er.y)))
                 return kStopTrap;
             if ((th.executed >= S.next || S.mode != 0) && !th.slow)
                 spin_at_entry(A, L, th, S);
@@ -1701,6 +1735,7 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
         const uint32_t P = static_cast<uint32_t>(A.n_params);
         L.code = A.insts + var.inst_base;
         L.suffix = A.suffix ? A.suffix + var.inst_base : nullptr;
+        L.edges = A.edges + var.inst_base;
         L.dblk = A.dblocks + var.block_base;
         L.arm = A.arms + var.arm_base;
         L.n_values = var.n_values;
@@ -1965,6 +2000,7 @@ __global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_
     if (active && S.state[j] != kInstDone) {
         L.code = A.insts + var.inst_base;
         L.suffix = A.suffix ? A.suffix + var.inst_base : nullptr;
+        L.edges = A.edges + var.inst_base;
         L.dblk = A.dblocks + var.block_base;
         L.arm = A.arms + var.arm_base;
         L.n_values = var.n_values;

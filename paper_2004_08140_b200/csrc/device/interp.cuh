@@ -23,6 +23,7 @@ struct InterpArgs {
     const gevo_block* blocks;
     const gevo_inst* insts;
     const gevo_arm* arms;
+    const gevo_edge* edges;        // [batch instruction] pre-resolved branch phis
     const uint32_t* lit_payload;
     const uint8_t* lit_tag;
     const uint4* dblocks;          // [batch block] {start, len | nphi << 16, cost (int64)}

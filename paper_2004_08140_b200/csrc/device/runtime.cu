@@ -221,6 +221,7 @@ void bind_batch(gevo::InterpArgs& A, const void* dblob, const gevo_batch_header&
     A.blocks = reinterpret_cast<const gevo_block*>(base + h.off_blocks);
     A.insts = reinterpret_cast<const gevo_inst*>(base + h.off_insts);
     A.arms = reinterpret_cast<const gevo_arm*>(base + h.off_arms);
+    A.edges = reinterpret_cast<const gevo_edge*>(base + h.off_edges);
     A.lit_payload = reinterpret_cast<const uint32_t*>(base + h.off_lit_payload);
     A.lit_tag = reinterpret_cast<const uint8_t*>(base + h.off_lit_tag);
     A.n_variants = h.n_variants;

@@ -337,8 +337,49 @@ void BatchImage::add(const Kernel& k) {
         blocks_.push_back(gb);
         rel += gb.len + 1u; // + fell-off sentinel
     }
+    // Branch edges: the target block's leading phis resolved for this block as
+    // predecessor (first arm whose label is this block, like enter_block).
+    auto edge_of = [&](int from_block, int target) -> std::pair<uint32_t, uint32_t> {
+        const std::pair<uint32_t, uint32_t> none{GEVO_EDGE_NONE, GEVO_EDGE_NONE};
+        if (target < 0 || static_cast<size_t>(target) >= k.blocks.size())
+            return none;
+        const BasicBlock& tb = k.blocks[static_cast<size_t>(target)];
+        uint32_t out[2] = {0, 0};
+        size_t nphi = 0;
+        while (nphi < tb.instructions.size() && tb.instructions[nphi].is_phi())
+            ++nphi;
+        if (nphi > 2)
+            return none;
+        for (size_t j = 0; j < nphi; ++j) {
+            const Instruction& phi = tb.instructions[j];
+            if (!phi.result || *phi.result < 0)
+                return none;
+            uint32_t r = GEVO_EDGE_NOINC;
+            const size_t n = std::min(phi.operands.size(), phi.labels.size());
+            for (size_t a = 0; a < n; ++a)
+                if (k.block_index(phi.labels[a]) == from_block) {
+                    r = ref(phi, a);
+                    break;
+                }
+            out[j] = r | (static_cast<uint32_t>(slot_of.at(*phi.result)) << 16);
+        }
+        return {out[0], out[1]};
+    };
+    int bidx = 0;
     for (const BasicBlock& blk : k.blocks) {
+        const int this_block = bidx++;
         for (const Instruction& in : blk.instructions) {
+            gevo_edge ge{};
+            if (in.op == Opcode::Br) {
+                for (size_t e = 0; e < 2; ++e) {
+                    const auto pr = e < in.labels.size()
+                                        ? edge_of(this_block, k.block_index(in.labels[e]))
+                                        : std::pair<uint32_t, uint32_t>{GEVO_EDGE_NONE, GEVO_EDGE_NONE};
+                    ge.phi[e][0] = pr.first;
+                    ge.phi[e][1] = pr.second;
+                }
+            }
+            edges_.push_back(ge);
             gevo_inst g{};
             g.op = static_cast<uint8_t>(in.op);
             g.cls = cost_class(k, in);
@@ -434,6 +475,7 @@ void BatchImage::add(const Kernel& k) {
         fell.res = GEVO_NO_RESULT;
         fell.t0 = fell.t1 = -1;
         insts_.push_back(fell);
+        edges_.push_back(gevo_edge{});
     }
     var.n_lits = static_cast<uint16_t>(n_lits);
     var.max_phis = static_cast<uint16_t>(max_phis);
@@ -488,6 +530,8 @@ const std::vector<uint8_t>& BatchImage::blob() {
     off = align(off + lit_payload_.size() * 4);
     h.off_lit_tag = off;
     off = align(off + lit_tag_.size());
+    h.off_edges = off;
+    off = align(off + edges_.size() * sizeof(gevo_edge));
     h.total_bytes = off;
     blob_.assign(off, 0);
     std::memcpy(blob_.data(), &h, sizeof h);
@@ -501,6 +545,7 @@ const std::vector<uint8_t>& BatchImage::blob() {
     put(h.off_arms, arms_.data(), arms_.size() * sizeof(gevo_arm));
     put(h.off_lit_payload, lit_payload_.data(), lit_payload_.size() * 4);
     put(h.off_lit_tag, lit_tag_.data(), lit_tag_.size());
+    put(h.off_edges, edges_.data(), edges_.size() * sizeof(gevo_edge));
     hdr_ = h;
     dirty_ = false;
     return blob_;

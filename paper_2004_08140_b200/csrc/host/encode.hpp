@@ -74,6 +74,7 @@ private:
     std::vector<gevo_variant> variants_;
     std::vector<gevo_block> blocks_;
     std::vector<gevo_inst> insts_;
+    std::vector<gevo_edge> edges_; // parallel to insts_
     std::vector<gevo_arm> arms_;
     std::vector<uint32_t> lit_payload_;
     std::vector<uint8_t> lit_tag_;
