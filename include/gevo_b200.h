@@ -46,6 +46,8 @@ typedef struct {
 #define GEVO_EVAL_TESTS 2u      /* fill per-test records */
 #define GEVO_EVAL_SEQUENTIAL 4u /* force the sequential-lane interpreter (one lane runs all
                                    simulated threads of an instance in id order) */
+#define GEVO_EVAL_UPLOAD 8u     /* gevo_eval_resident_async: copy the batch's host bytecode
+                                   to the device as part of this evaluation */
 
 typedef struct {
     float device_ms;       /* CUDA-event time of the interpreter + reduction launches */
@@ -127,6 +129,17 @@ int gevo_eval(gevo_batch* b, const gevo_exec_config* cfg, double tolerance, uint
 int gevo_batch_make_resident(gevo_batch* b);
 int gevo_eval_resident(gevo_batch* b, const gevo_exec_config* cfg, double tolerance,
                        uint32_t flags, gevo_variant_record* out_variants, gevo_eval_stats* stats);
+/* Concurrent evaluation of resident batches: _async launches the batch on its
+ * own stream (after the work already queued on the library's current stream,
+ * which in turn waits for it) and returns; _wait blocks until it finishes and
+ * returns its records and device time. Several batches in flight overlap on
+ * the GPU (their launch tails run side by side). One evaluation in flight per
+ * batch. No reference counterpart (the reference evaluates one kernel at a
+ * time). */
+int gevo_eval_resident_async(gevo_batch* b, const gevo_exec_config* cfg, double tolerance,
+                             uint32_t flags);
+int gevo_eval_resident_wait(gevo_batch* b, gevo_variant_record* out_variants,
+                            gevo_eval_stats* stats);
 /* Reference reason string of a record (ExecResult::trap_reason /
  * EvalOutcome::reason, src/vm.cpp:513-571). */
 int gevo_reason(const gevo_batch* b, int variant, uint32_t code, int32_t aux, double fail_error,

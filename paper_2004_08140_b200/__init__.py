@@ -31,7 +31,7 @@ assert TEST_RECORD.itemsize == 32 and VARIANT_RECORD.itemsize == 48
 
 STATUS_COMPLETED, STATUS_TRAP, STATUS_BUDGET, STATUS_SKIPPED = 0, 1, 2, 3
 FAIL_TOLERANCE = 0xFF
-EVAL_EARLY_EXIT, EVAL_TESTS, EVAL_SEQUENTIAL = 1, 2, 4
+EVAL_EARLY_EXIT, EVAL_TESTS, EVAL_SEQUENTIAL, EVAL_UPLOAD = 1, 2, 4, 8
 COST_FIELDS = ("arith", "cmp", "select_op", "phi", "constant", "br", "intrinsic", "getindex",
                "load_shared", "store_shared", "load_global", "store_global", "sync", "ret")
 DEFAULT_COSTS = (1, 1, 1, 1, 1, 1, 1, 1, 4, 4, 20, 20, 8, 1)
@@ -115,6 +115,8 @@ _SIGNATURES = [
     ("gevo_eval", ctypes.c_int, [_vp, ctypes.POINTER(ExecConfig), _f64, _u32, _vp, _vp,
                                  ctypes.POINTER(EvalStats)]),
     ("gevo_batch_make_resident", ctypes.c_int, [_vp]),
+    ("gevo_eval_resident_async", ctypes.c_int, [_vp, ctypes.POINTER(ExecConfig), _f64, _u32]),
+    ("gevo_eval_resident_wait", ctypes.c_int, [_vp, _vp, ctypes.POINTER(EvalStats)]),
     ("gevo_eval_resident", ctypes.c_int, [_vp, ctypes.POINTER(ExecConfig), _f64, _u32, _vp,
                                           ctypes.POINTER(EvalStats)]),
     ("gevo_reason", ctypes.c_int, [_vp, ctypes.c_int, _u32, _i32, _f64, _str_out]),
@@ -401,6 +403,22 @@ class Batch:
 
     def make_resident(self):
         _check(lib().gevo_batch_make_resident(self._h))
+
+    def eval_resident_async(self, cfg: ExecConfig, tolerance: float = 0.0,
+                            early_exit: bool = True, upload: bool = False) -> None:
+        """Launch on the batch's own stream and return (overlaps with other
+        batches in flight); pair with wait(). upload=True copies the host
+        bytecode to the device as part of the evaluation."""
+        flags = (EVAL_EARLY_EXIT if early_exit else 0) | (EVAL_UPLOAD if upload else 0)
+        _check(lib().gevo_eval_resident_async(self._h, ctypes.byref(cfg), tolerance, flags))
+
+    def wait(self, records: bool = True):
+        """(variant records | None, EvalStats) of the evaluation in flight."""
+        vrec = np.zeros(len(self), VARIANT_RECORD) if records else None
+        st = EvalStats()
+        _check(lib().gevo_eval_resident_wait(
+            self._h, vrec.ctypes.data_as(ctypes.c_void_p) if records else None, ctypes.byref(st)))
+        return vrec, st
 
     def eval_resident(self, cfg: ExecConfig, tolerance: float = 0.0, early_exit: bool = True,
                       records: bool = False):

@@ -267,6 +267,35 @@ int gevo_eval(gevo_batch* b, const gevo_exec_config* cfg, double tolerance, uint
     });
 }
 
+int gevo_eval_resident_async(gevo_batch* b, const gevo_exec_config* cfg, double tolerance,
+                             uint32_t flags) {
+    return guard([&] {
+        const bool upload = (flags & GEVO_EVAL_UPLOAD) != 0;
+        if (!b->resident)
+            b->resident = b200::make_resident(*b->suite->suite, *b->image);
+        b200::EvalOptions opt;
+        opt.tolerance = tolerance;
+        opt.early_exit = (flags & GEVO_EVAL_EARLY_EXIT) != 0;
+        opt.sequential = (flags & GEVO_EVAL_SEQUENTIAL) != 0;
+        b200::evaluate_resident_async(*b->resident, b200::exec_image(exec_from(cfg)), opt,
+                                      upload ? &b->image->blob() : nullptr);
+    });
+}
+
+int gevo_eval_resident_wait(gevo_batch* b, gevo_variant_record* out_variants, gevo_eval_stats* stats) {
+    return guard([&] {
+        if (!b->resident)
+            throw std::invalid_argument("batch is not resident");
+        std::vector<gevo_variant_record> recs;
+        int launches = 0;
+        const float ms = b200::wait_resident(*b->resident, out_variants ? &recs : nullptr, &launches);
+        if (out_variants && !recs.empty())
+            std::memcpy(out_variants, recs.data(), recs.size() * sizeof(gevo_variant_record));
+        fill_stats(stats, ms, b200::resident_h2d(*b->resident),
+                   recs.size() * sizeof(gevo_variant_record), launches);
+    });
+}
+
 int gevo_batch_make_resident(gevo_batch* b) {
     return guard([&] { b->resident = b200::make_resident(*b->suite->suite, *b->image); });
 }

@@ -65,19 +65,26 @@ struct PinnedBuf {
 
 } // namespace
 
+// Device scratch of one evaluation stream: records, per-instance memory,
+// spin-accelerator state. The device owns one (synchronous calls); every
+// resident batch owns another, so batches can be evaluated concurrently on
+// their own streams.
+struct Scratch {
+    DevBuf rec, vrec, first_fail, priv, sh_tag, sh_val;
+    DevBuf ts_pos, ts_prev, ts_exec, ts_stop, ts_val, ts_tag;
+    DevBuf tp_snap, gcells, gshadow, outcells, suffix, sp_vk;
+    DevBuf bcost, vf, sp_base, sp_btag, sp_delta, sp_cur, sp_hvary, sp_cvary, sp_log, sp_ld;
+    size_t scratch_budget = size_t(8) << 30; // bytes of per-instance scratch per launch
+};
+
 struct DeviceImpl {
     int ordinal = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr; // created here; `stream` may be a caller's
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
-    DevBuf blob, rec, vrec, first_fail, priv, sh_tag, sh_val;
-    DevBuf ts_pos, ts_prev, ts_exec, ts_stop, ts_val, ts_tag;
-    DevBuf tp_snap, gcells, gshadow, outcells, suffix, sp_vk;
-    DevBuf bcost, vf, sp_base, sp_btag, sp_delta, sp_cur, sp_hvary, sp_cvary, sp_log, sp_ld,
-        counters;
-    DevBuf rank;
+    DevBuf blob, counters, rank;
+    Scratch sc;
     PinnedBuf h_blob, h_vrec, h_rec;
-    size_t scratch_budget = size_t(8) << 30; // bytes of per-instance scratch per launch
 };
 
 struct SuiteImpl {
@@ -251,30 +258,30 @@ bool tp_enabled() {
 }
 
 // Spin-accelerator scratch for `cols` columns (instances or lanes).
-void reserve_spin(DeviceImpl& dev, gevo::InterpArgs& A, size_t cols) {
+void reserve_spin(Scratch& sc, gevo::InterpArgs& A, size_t cols) {
     const size_t n = cols * A.max_slots;
-    dev.sp_base.reserve(n * 4);
-    dev.sp_btag.reserve(n);
-    dev.sp_delta.reserve(n * 4);
-    dev.sp_cur.reserve(n * 4);
-    dev.sp_hvary.reserve(n);
-    dev.sp_cvary.reserve(n);
-    dev.sp_log.reserve(cols * gevo::kSpinLog * 5 * 4);
-    dev.sp_ld.reserve(cols * gevo::kSpinLog * 4);
-    dev.sp_vk.reserve(cols * gevo::kSpinLog * 4);
-    A.sp_vk = dev.sp_vk.as<uint32_t>();
-    A.sp_hvary = dev.sp_hvary.as<uint8_t>();
-    A.sp_cvary = dev.sp_cvary.as<uint8_t>();
-    A.sp_log = dev.sp_log.as<uint32_t>();
-    A.sp_ld = dev.sp_ld.as<uint32_t>();
-    A.sp_base = dev.sp_base.as<uint32_t>();
-    A.sp_btag = dev.sp_btag.as<uint8_t>();
-    A.sp_delta = dev.sp_delta.as<uint32_t>();
-    A.sp_cur = dev.sp_cur.as<uint32_t>();
+    sc.sp_base.reserve(n * 4);
+    sc.sp_btag.reserve(n);
+    sc.sp_delta.reserve(n * 4);
+    sc.sp_cur.reserve(n * 4);
+    sc.sp_hvary.reserve(n);
+    sc.sp_cvary.reserve(n);
+    sc.sp_log.reserve(cols * gevo::kSpinLog * 5 * 4);
+    sc.sp_ld.reserve(cols * gevo::kSpinLog * 4);
+    sc.sp_vk.reserve(cols * gevo::kSpinLog * 4);
+    A.sp_vk = sc.sp_vk.as<uint32_t>();
+    A.sp_hvary = sc.sp_hvary.as<uint8_t>();
+    A.sp_cvary = sc.sp_cvary.as<uint8_t>();
+    A.sp_log = sc.sp_log.as<uint32_t>();
+    A.sp_ld = sc.sp_ld.as<uint32_t>();
+    A.sp_base = sc.sp_base.as<uint32_t>();
+    A.sp_btag = sc.sp_btag.as<uint8_t>();
+    A.sp_delta = sc.sp_delta.as<uint32_t>();
+    A.sp_cur = sc.sp_cur.as<uint32_t>();
 }
 
 // Launches the interpreter over all variants in scratch-bounded chunks, then
-// the per-variant reduction. Records land in dev.rec / dev.vrec.
+// the per-variant reduction. Records land in dev.sc.rec / dev.sc.vrec.
 // Where the final global buffers of the instances are after a launch
 // (want_outputs): the sequential kernel's private copies (u32 words) or the
 // thread-parallel kernel's memory cells (uint2, payload in .x); element e of
@@ -286,7 +293,7 @@ struct OutputWindow {
     std::vector<size_t> off;
 };
 
-int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const gevo_batch_header& h,
+int launch_all(DeviceImpl& dev, Scratch& sc, DeviceSuite& suite, gevo::InterpArgs A, const gevo_batch_header& h,
                uint64_t writable_any, const ExecImage& ex, const EvalOptions& opt,
                cudaStream_t s, OutputWindow* ow = nullptr) {
     const SuiteImage& S = suite.image();
@@ -294,25 +301,25 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
         throw std::invalid_argument("variant value file exceeds the device limit");
     const uint32_t T = static_cast<uint32_t>(std::max(S.n_tests, 1));
     const uint64_t total = static_cast<uint64_t>(h.n_variants) * static_cast<uint64_t>(S.n_tests);
-    dev.rec.reserve(std::max<size_t>(total * sizeof(gevo_test_record), 16));
-    dev.vrec.reserve(std::max<size_t>(h.n_variants * sizeof(gevo_variant_record), 16));
-    dev.first_fail.reserve(std::max<size_t>(h.n_variants * sizeof(int32_t), 16));
+    sc.rec.reserve(std::max<size_t>(total * sizeof(gevo_test_record), 16));
+    sc.vrec.reserve(std::max<size_t>(h.n_variants * sizeof(gevo_variant_record), 16));
+    sc.first_fail.reserve(std::max<size_t>(h.n_variants * sizeof(int32_t), 16));
     if (opt.early_exit)
-        check(cudaMemsetAsync(dev.first_fail.ptr, 0x7f, h.n_variants * sizeof(int32_t), s),
+        check(cudaMemsetAsync(sc.first_fail.ptr, 0x7f, h.n_variants * sizeof(int32_t), s),
               "memset first_fail");
-    A.rec = dev.rec.as<gevo_test_record>();
-    A.first_fail = dev.first_fail.as<int32_t>();
+    A.rec = sc.rec.as<gevo_test_record>();
+    A.first_fail = sc.first_fail.as<int32_t>();
     int launches = 0;
 
     // Block costs under this launch's cost table.
-    dev.bcost.reserve(std::max<size_t>(h.n_blocks * sizeof(uint4), 16));
-    dev.suffix.reserve(std::max<size_t>(h.n_insts * sizeof(int64_t), 16));
+    sc.bcost.reserve(std::max<size_t>(h.n_blocks * sizeof(uint4), 16));
+    sc.suffix.reserve(std::max<size_t>(h.n_insts * sizeof(int64_t), 16));
     check(gevo::launch_block_cost(A.blocks, A.insts, A.variants, h.n_variants, ex.cost.data(),
-                                  dev.bcost.as<uint4>(), dev.suffix.as<int64_t>(), s),
+                                  sc.bcost.as<uint4>(), sc.suffix.as<int64_t>(), s),
           "block_cost_kernel launch");
     ++launches;
-    A.dblocks = dev.bcost.as<uint4>();
-    A.suffix = dev.suffix.as<int64_t>();
+    A.dblocks = sc.bcost.as<uint4>();
+    A.suffix = sc.suffix.as<int64_t>();
 
     const int64_t thr = spin_threshold();
     if (!dev.counters.ptr) {
@@ -350,13 +357,13 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
         // global cells + access records: 16 bytes per cell per instance
         const size_t per_variant = std::max<size_t>(per_lane, 1) * lanes_per_variant +
                                    (gc ? 16 * static_cast<size_t>(n_cells) * T : 0);
-        size_t chunk = std::max<size_t>(dev.scratch_budget / per_variant, 1);
+        size_t chunk = std::max<size_t>(sc.scratch_budget / per_variant, 1);
         chunk = std::min<size_t>(chunk, std::max<uint32_t>(h.n_variants, 1));
         if (opt.want_outputs)
             chunk = std::max<uint32_t>(h.n_variants, 1); // one launch window
         const size_t lanes = chunk * lanes_per_variant;
         if (thr > 0) {
-            reserve_spin(dev, A, lanes);
+            reserve_spin(sc, A, lanes);
             A.spin_threshold = thr;
         }
         A.tp_snap = nullptr;
@@ -365,19 +372,19 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
         A.gshadow = nullptr;
         if (gc) {
             const size_t cells = std::max<size_t>(static_cast<size_t>(n_cells) * chunk * T, 1);
-            dev.gcells.reserve(cells * 8);
-            dev.gshadow.reserve(cells * 8);
-            A.gcells = dev.gcells.as<uint2>();
-            A.gshadow = dev.gshadow.as<unsigned long long>();
+            sc.gcells.reserve(cells * 8);
+            sc.gshadow.reserve(cells * 8);
+            A.gcells = sc.gcells.as<uint2>();
+            A.gshadow = sc.gshadow.as<unsigned long long>();
         } else if (h.any_sync) {
-            dev.tp_snap.reserve(lanes * std::max<uint32_t>(h.max_values, 1) * 8);
-            A.tp_snap = dev.tp_snap.as<uint2>();
+            sc.tp_snap.reserve(lanes * std::max<uint32_t>(h.max_values, 1) * 8);
+            A.tp_snap = sc.tp_snap.as<uint2>();
         }
         if (opt.want_outputs && ow) {
             const size_t n_inst = static_cast<size_t>(h.n_variants) * T;
             if (!gc) {
-                dev.outcells.reserve(std::max<size_t>(static_cast<size_t>(n_cells) * n_inst * 8, 16));
-                A.out_cells = dev.outcells.as<uint2>();
+                sc.outcells.reserve(std::max<size_t>(static_cast<size_t>(n_cells) * n_inst * 8, 16));
+                A.out_cells = sc.outcells.as<uint2>();
             }
             ow->mode = 2;
             ow->ptr = gc ? static_cast<const void*>(A.gcells) : static_cast<const void*>(A.out_cells);
@@ -398,8 +405,8 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
             check(gevo::launch_interp_tp(L, s), "interp_tp_kernel launch");
             ++launches;
         }
-        check(gevo::launch_fitness(dev.rec.as<gevo_test_record>(), h.n_variants, S.n_tests,
-                                   opt.tolerance, dev.vrec.as<gevo_variant_record>(), s),
+        check(gevo::launch_fitness(sc.rec.as<gevo_test_record>(), h.n_variants, S.n_tests,
+                                   opt.tolerance, sc.vrec.as<gevo_variant_record>(), s),
               "fitness_kernel launch");
         return launches + 1;
     }
@@ -414,48 +421,48 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
                              shape.vf_global),
         1);
     // chunk = variants per launch
-    size_t chunk = std::max<size_t>(dev.scratch_budget / (per * T), 64);
+    size_t chunk = std::max<size_t>(sc.scratch_budget / (per * T), 64);
     chunk = std::min<size_t>(chunk, std::max<uint32_t>(h.n_variants, 1));
     const size_t cap = chunk * T; // instances per launch window
     size_t priv_words = 0;
     for (int p = 0; p < S.n_params; ++p)
         if ((writable_any >> p) & 1ull)
             priv_words += static_cast<size_t>(S.pool_rows[static_cast<size_t>(p)]);
-    dev.priv.reserve(std::max<size_t>(priv_words * cap * 4, 16));
+    sc.priv.reserve(std::max<size_t>(priv_words * cap * 4, 16));
     const size_t sw = static_cast<size_t>(std::max(ex.shared_words, 0));
-    dev.sh_tag.reserve(std::max<size_t>(sw * cap, 16));
-    dev.sh_val.reserve(std::max<size_t>(sw * cap * 4, 16));
-    A.priv = dev.priv.as<uint32_t>();
-    A.sh_tag = dev.sh_tag.as<uint8_t>();
-    A.sh_val = dev.sh_val.as<uint32_t>();
+    sc.sh_tag.reserve(std::max<size_t>(sw * cap, 16));
+    sc.sh_val.reserve(std::max<size_t>(sw * cap * 4, 16));
+    A.priv = sc.priv.as<uint32_t>();
+    A.sh_tag = sc.sh_tag.as<uint8_t>();
+    A.sh_val = sc.sh_val.as<uint32_t>();
     if (h.any_sync) {
         const size_t tn = static_cast<size_t>(ex.threads) * cap;
-        dev.ts_pos.reserve(tn * 4);
-        dev.ts_prev.reserve(tn * 4);
-        dev.ts_exec.reserve(tn * 8);
-        dev.ts_stop.reserve(tn * 4);
-        dev.ts_val.reserve(tn * A.ts_slots * 4);
-        dev.ts_tag.reserve(tn * A.ts_slots);
-        A.ts_pos = dev.ts_pos.as<int32_t>();
-        A.ts_prev = dev.ts_prev.as<int32_t>();
-        A.ts_exec = dev.ts_exec.as<int64_t>();
-        A.ts_stop = dev.ts_stop.as<uint32_t>();
-        A.ts_val = dev.ts_val.as<uint32_t>();
-        A.ts_tag = dev.ts_tag.as<uint8_t>();
+        sc.ts_pos.reserve(tn * 4);
+        sc.ts_prev.reserve(tn * 4);
+        sc.ts_exec.reserve(tn * 8);
+        sc.ts_stop.reserve(tn * 4);
+        sc.ts_val.reserve(tn * A.ts_slots * 4);
+        sc.ts_tag.reserve(tn * A.ts_slots);
+        A.ts_pos = sc.ts_pos.as<int32_t>();
+        A.ts_prev = sc.ts_prev.as<int32_t>();
+        A.ts_exec = sc.ts_exec.as<int64_t>();
+        A.ts_stop = sc.ts_stop.as<uint32_t>();
+        A.ts_val = sc.ts_val.as<uint32_t>();
+        A.ts_tag = sc.ts_tag.as<uint8_t>();
     }
     if (shape.vf_global) {
-        dev.vf.reserve(cap * A.max_slots * 8);
-        A.vf = dev.vf.as<uint2>();
+        sc.vf.reserve(cap * A.max_slots * 8);
+        A.vf = sc.vf.as<uint2>();
     }
     if (thr > 0) {
-        reserve_spin(dev, A, cap);
+        reserve_spin(sc, A, cap);
         A.spin_threshold = thr;
     }
     if (opt.want_outputs && ow) {
         if (chunk < h.n_variants)
             throw std::invalid_argument("want_outputs needs a single-launch batch");
         ow->mode = 1;
-        ow->ptr = dev.priv.ptr;
+        ow->ptr = sc.priv.ptr;
         ow->n_inst = static_cast<size_t>(h.n_variants) * T;
         ow->off.assign(static_cast<size_t>(S.n_params), 0);
         size_t words = 0;
@@ -481,8 +488,8 @@ int launch_all(DeviceImpl& dev, DeviceSuite& suite, gevo::InterpArgs A, const ge
         check(gevo::launch_interp(L, s), "interp_kernel launch");
         ++launches;
     }
-    check(gevo::launch_fitness(dev.rec.as<gevo_test_record>(), h.n_variants, S.n_tests,
-                               opt.tolerance, dev.vrec.as<gevo_variant_record>(), s),
+    check(gevo::launch_fitness(sc.rec.as<gevo_test_record>(), h.n_variants, S.n_tests,
+                               opt.tolerance, sc.vrec.as<gevo_variant_record>(), s),
           "fitness_kernel launch");
     return launches + 1;
 }
@@ -523,12 +530,12 @@ EvalResult evaluate(DeviceSuite& suite, BatchImage& batch, const ExecImage& exec
     bind_batch(A, dev.blob.ptr, h);
     check(cudaEventRecord(dev.ev1, s), "event");
     OutputWindow ow;
-    R.launches = launch_all(dev, suite, A, h, wr, exec, opt, s, &ow);
+    R.launches = launch_all(dev, dev.sc, suite, A, h, wr, exec, opt, s, &ow);
     check(cudaEventRecord(dev.ev2, s), "event");
 
     R.variants.resize(h.n_variants);
     if (h.n_variants) {
-        check(cudaMemcpyAsync(R.variants.data(), dev.vrec.ptr,
+        check(cudaMemcpyAsync(R.variants.data(), dev.sc.vrec.ptr,
                               h.n_variants * sizeof(gevo_variant_record), cudaMemcpyDeviceToHost, s),
               "records D2H");
         R.d2h_bytes += h.n_variants * sizeof(gevo_variant_record);
@@ -537,7 +544,7 @@ EvalResult evaluate(DeviceSuite& suite, BatchImage& batch, const ExecImage& exec
     if (opt.want_tests || opt.want_outputs) {
         R.tests.resize(total);
         if (total)
-            check(cudaMemcpyAsync(R.tests.data(), dev.rec.ptr, total * sizeof(gevo_test_record),
+            check(cudaMemcpyAsync(R.tests.data(), dev.sc.rec.ptr, total * sizeof(gevo_test_record),
                                   cudaMemcpyDeviceToHost, s),
                   "test records D2H");
         R.d2h_bytes += total * sizeof(gevo_test_record);
@@ -601,6 +608,24 @@ struct ResidentBatch {
     DevBuf blob;
     gevo_batch_header h;
     uint64_t writable;
+    // concurrent evaluation: own stream, scratch and record staging
+    cudaStream_t stream = nullptr;
+    cudaEvent_t origin = nullptr, start = nullptr, done = nullptr;
+    Scratch sc;
+    PinnedBuf h_vrec, h_blob;
+    int launches = 0;
+    uint64_t h2d = 0; // bytes uploaded by the evaluation in flight
+    bool pending = false;
+    ~ResidentBatch() {
+        if (stream)
+            cudaStreamDestroy(stream);
+        if (origin)
+            cudaEventDestroy(origin);
+        if (start)
+            cudaEventDestroy(start);
+        if (done)
+            cudaEventDestroy(done);
+    }
 };
 
 std::shared_ptr<ResidentBatch> make_resident(DeviceSuite& suite, BatchImage& batch) {
@@ -617,6 +642,70 @@ std::shared_ptr<ResidentBatch> make_resident(DeviceSuite& suite, BatchImage& bat
     return rb;
 }
 
+void evaluate_resident_async(ResidentBatch& rb, const ExecImage& exec, const EvalOptions& opt,
+                             const std::vector<uint8_t>* upload) {
+    Device& devh = rb.suite->device();
+    std::lock_guard<std::mutex> g(devh.lock());
+    DeviceImpl& dev = devh.impl();
+    check(cudaSetDevice(dev.ordinal), "cudaSetDevice");
+    if (rb.pending)
+        throw std::logic_error("resident batch already has an evaluation in flight");
+    if (!rb.stream) {
+        check(cudaStreamCreateWithFlags(&rb.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        check(cudaEventCreateWithFlags(&rb.origin, cudaEventDisableTiming), "cudaEventCreate");
+        check(cudaEventCreate(&rb.start), "cudaEventCreate");
+        check(cudaEventCreate(&rb.done), "cudaEventCreate");
+    }
+    // ordered after the caller's stream (its CUDA events bracket the work)
+    check(cudaEventRecord(rb.origin, dev.stream), "event");
+    check(cudaStreamWaitEvent(rb.stream, rb.origin, 0), "stream wait");
+    check(cudaEventRecord(rb.start, rb.stream), "event");
+    rb.h2d = upload ? upload->size() : 0;
+    if (upload) {
+        // host bytecode of the batch, copied in this evaluation (end-to-end form)
+        rb.h_blob.reserve(upload->size());
+        std::memcpy(rb.h_blob.ptr, upload->data(), upload->size());
+        check(cudaMemcpyAsync(rb.blob.ptr, rb.h_blob.ptr, upload->size(), cudaMemcpyHostToDevice,
+                              rb.stream),
+              "blob H2D");
+    }
+    gevo::InterpArgs A = base_args(*rb.suite, exec, opt);
+    bind_batch(A, rb.blob.ptr, rb.h);
+    rb.launches = launch_all(dev, rb.sc, *rb.suite, A, rb.h, rb.writable, exec, opt, rb.stream);
+    const size_t nb = rb.h.n_variants * sizeof(gevo_variant_record);
+    rb.h_vrec.reserve(std::max<size_t>(nb, 16));
+    if (nb)
+        check(cudaMemcpyAsync(rb.h_vrec.ptr, rb.sc.vrec.ptr, nb, cudaMemcpyDeviceToHost, rb.stream),
+              "records");
+    check(cudaEventRecord(rb.done, rb.stream), "event");
+    // (the caller's stream is ordered after `done` by wait_resident, not here:
+    // a second batch launched now must not queue behind this one)
+    rb.pending = true;
+}
+
+uint64_t resident_h2d(const ResidentBatch& rb) { return rb.h2d; }
+
+float wait_resident(ResidentBatch& rb, std::vector<gevo_variant_record>* out, int* launches) {
+    if (!rb.pending)
+        throw std::logic_error("no evaluation in flight");
+    check(cudaEventSynchronize(rb.done), "resident eval");
+    {
+        Device& devh = rb.suite->device();
+        std::lock_guard<std::mutex> g(devh.lock());
+        check(cudaStreamWaitEvent(devh.impl().stream, rb.done, 0), "stream wait");
+    }
+    rb.pending = false;
+    float ms = 0;
+    check(cudaEventElapsedTime(&ms, rb.start, rb.done), "elapsed");
+    if (out) {
+        out->resize(rb.h.n_variants);
+        std::memcpy(out->data(), rb.h_vrec.ptr, rb.h.n_variants * sizeof(gevo_variant_record));
+    }
+    if (launches)
+        *launches = rb.launches;
+    return ms;
+}
+
 float evaluate_resident(ResidentBatch& rb, const ExecImage& exec, const EvalOptions& opt,
                         float* interp_ms, std::vector<gevo_variant_record>* out, int* launches) {
     Device& devh = rb.suite->device();
@@ -627,13 +716,13 @@ float evaluate_resident(ResidentBatch& rb, const ExecImage& exec, const EvalOpti
     gevo::InterpArgs A = base_args(*rb.suite, exec, opt);
     bind_batch(A, rb.blob.ptr, rb.h);
     check(cudaEventRecord(dev.ev0, s), "event");
-    const int nl = launch_all(dev, *rb.suite, A, rb.h, rb.writable, exec, opt, s);
+    const int nl = launch_all(dev, dev.sc, *rb.suite, A, rb.h, rb.writable, exec, opt, s);
     if (launches)
         *launches = nl;
     check(cudaEventRecord(dev.ev2, s), "event");
     if (out) {
         out->resize(rb.h.n_variants);
-        check(cudaMemcpyAsync(out->data(), dev.vrec.ptr, rb.h.n_variants * sizeof(gevo_variant_record),
+        check(cudaMemcpyAsync(out->data(), dev.sc.vrec.ptr, rb.h.n_variants * sizeof(gevo_variant_record),
                               cudaMemcpyDeviceToHost, s),
               "records");
     }

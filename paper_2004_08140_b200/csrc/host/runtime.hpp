@@ -81,6 +81,16 @@ std::shared_ptr<ResidentBatch> make_resident(DeviceSuite& suite, BatchImage& bat
 // Runs the interpreter + reduction on a resident batch; returns kernel ms
 // (CUDA events on the launch stream) and fills `interp_ms` with the share of
 // the interpreter kernel alone.
+// Concurrent form: launches on the batch's own stream (ordered after the work
+// queued on the device's current stream) and returns; wait_resident blocks,
+// orders the current stream after the batch and returns its device ms.
+// Batches evaluated this way overlap on the GPU.
+// `upload` (nullable): the batch's host bytecode, copied H2D as part of the
+// evaluation (the blob must be the one the batch was made resident with).
+void evaluate_resident_async(ResidentBatch& rb, const ExecImage& exec, const EvalOptions& opt,
+                             const std::vector<uint8_t>* upload = nullptr);
+float wait_resident(ResidentBatch& rb, std::vector<gevo_variant_record>* out, int* launches);
+uint64_t resident_h2d(const ResidentBatch& rb);
 float evaluate_resident(ResidentBatch& rb, const ExecImage& exec, const EvalOptions& opt,
                         float* interp_ms, std::vector<gevo_variant_record>* out,
                         int* launches = nullptr);
