@@ -494,6 +494,32 @@ void BatchImage::add(const Kernel& k) {
     dirty_ = true;
 }
 
+void BatchImage::append(BatchImage&& o) {
+    const uint32_t ib = static_cast<uint32_t>(insts_.size()), bb = static_cast<uint32_t>(blocks_.size());
+    const uint32_t ab = static_cast<uint32_t>(arms_.size()), lb = static_cast<uint32_t>(lit_payload_.size());
+    for (gevo_variant v : o.variants_) {
+        v.inst_base += ib;
+        v.block_base += bb;
+        v.arm_base += ab;
+        v.lit_base += lb;
+        variants_.push_back(v);
+    }
+    blocks_.insert(blocks_.end(), o.blocks_.begin(), o.blocks_.end());
+    insts_.insert(insts_.end(), o.insts_.begin(), o.insts_.end());
+    edges_.insert(edges_.end(), o.edges_.begin(), o.edges_.end());
+    arms_.insert(arms_.end(), o.arms_.begin(), o.arms_.end());
+    lit_payload_.insert(lit_payload_.end(), o.lit_payload_.begin(), o.lit_payload_.end());
+    lit_tag_.insert(lit_tag_.end(), o.lit_tag_.begin(), o.lit_tag_.end());
+    for (auto& sv : o.slot_value_)
+        slot_value_.push_back(std::move(sv));
+    max_slots_ = std::max(max_slots_, o.max_slots_);
+    max_values_ = std::max(max_values_, o.max_values_);
+    max_lits_ = std::max(max_lits_, o.max_lits_);
+    max_lane_slots_ = std::max(max_lane_slots_, o.max_lane_slots_);
+    any_sync_ = any_sync_ || o.any_sync_;
+    dirty_ = true;
+}
+
 const gevo_batch_header& BatchImage::header() {
     blob();
     return hdr_;

@@ -56,6 +56,9 @@ public:
     // Appends one variant; throws std::invalid_argument on an unsupported
     // shape (different parameter list than the suite, > GEVO_MAX_SLOTS slots).
     void add(const Kernel& k);
+    // Moves every variant of `other` (same suite) to the end of this batch.
+    // Lets a large batch be encoded in parallel parts and joined in order.
+    void append(BatchImage&& other);
     size_t size() const { return variants_.size(); }
 
     // Contiguous blob in the bytecode.h layout.

@@ -96,7 +96,7 @@ int wave_size(int used, int retries) {
 // [begin_r, end_r) of the batch and the records are all-gathered.
 std::vector<EvalOutcome> device_verdicts(b200::DeviceSuite& suite, const b200::ExecImage& ex,
                                          const std::vector<const Kernel*>& ks, double tol,
-                                         bool with_reasons, EngineCounters& ctr) {
+                                         bool with_reasons, EngineCounters& ctr, int jobs = 1) {
     std::vector<EvalOutcome> out(ks.size());
     if (ks.empty())
         return out;
@@ -115,9 +115,27 @@ std::vector<EvalOutcome> device_verdicts(b200::DeviceSuite& suite, const b200::E
         return std::make_pair(b, b + q + (r < m ? 1 : 0));
     };
     const auto [lo, hi] = span(R);
+    // encode in parallel parts (the device bytecode of ~10^5 candidates per
+    // search is otherwise a serial host term), joined in candidate order
+    const auto t_enc = std::chrono::steady_clock::now();
     b200::BatchImage batch(suite.image());
-    for (size_t v = lo; v < hi; ++v)
-        batch.add(*ks[v]);
+    constexpr size_t kPart = 64;
+    const size_t parts = (hi - lo + kPart - 1) / kPart;
+    if (jobs > 1 && parts > 1) {
+        std::vector<std::unique_ptr<b200::BatchImage>> part(parts);
+        host_parallel(parts, jobs, [&](size_t p) {
+            part[p] = std::make_unique<b200::BatchImage>(suite.image());
+            for (size_t v = lo + p * kPart; v < std::min(hi, lo + (p + 1) * kPart); ++v)
+                part[p]->add(*ks[v]);
+        });
+        for (auto& p : part)
+            batch.append(std::move(*p));
+    } else {
+        for (size_t v = lo; v < hi; ++v)
+            batch.add(*ks[v]);
+    }
+    batch.blob(); // serialise here, so the encode time below covers it
+    ctr.host_gen_ms += ms_since(t_enc);
     b200::EvalOptions opt;
     opt.tolerance = tol;
     opt.early_exit = true;
@@ -253,7 +271,7 @@ std::vector<EvalOutcome> Engine::sanity_check_batch(const std::vector<const Kern
         dev.push_back(ks[i]);
         where.push_back(i);
     }
-    const auto v = device_verdicts(*suite_, *exec_img_, dev, cfg_.tolerance, with_reasons, counters_);
+    const auto v = device_verdicts(*suite_, *exec_img_, dev, cfg_.tolerance, with_reasons, counters_, cfg_.jobs);
     for (size_t j = 0; j < where.size(); ++j)
         out[where[j]] = v[j];
     return out;
@@ -311,7 +329,7 @@ void Engine::run_mutations(std::vector<MutJob>& jobs) const {
                 }
         counters_.host_gen_ms += ms_since(t0);
         const auto verdicts =
-            device_verdicts(*suite_, *exec_img_, ks, cfg_.tolerance, false, counters_);
+            device_verdicts(*suite_, *exec_img_, ks, cfg_.tolerance, false, counters_, cfg_.jobs);
         // 3. resolve each slot in attempt order
         for (MutJob* j : active) {
             for (auto& at : j->wave) {
@@ -392,7 +410,7 @@ void Engine::run_crossovers(std::vector<CxJob>& jobs) const {
             }
         counters_.host_gen_ms += ms_since(t0);
         const auto verdicts =
-            device_verdicts(*suite_, *exec_img_, ks, cfg_.tolerance, false, counters_);
+            device_verdicts(*suite_, *exec_img_, ks, cfg_.tolerance, false, counters_, cfg_.jobs);
         for (CxJob* j : active) {
             for (auto& at : j->wave) {
                 ++j->used;
@@ -676,7 +694,7 @@ SearchResult Engine::run(const std::vector<TestCase>& heldout) {
         std::vector<const Kernel*> ks;
         for (const auto& e : archive_)
             ks.push_back(&e.ind.kernel);
-        const auto v = device_verdicts(hs, *exec_img_, ks, cfg_.tolerance, false, counters_);
+        const auto v = device_verdicts(hs, *exec_img_, ks, cfg_.tolerance, false, counters_, cfg_.jobs);
         for (size_t i = 0; i < archive_.size(); ++i) {
             if (v[i].accepted) {
                 archive_[i].heldout_error = v[i].fitness.error;
