@@ -203,7 +203,7 @@ struct Lane {
     uint32_t v, t, il;
     uint32_t sl;     // spin-accelerator scratch column (instance, or lane when kTP)
     int32_t tid;
-    const uint32_t* binfo;   // [param] size << 8 | elem of this lane's test
+    const uint2* binfo;      // [param] {size << 8 | elem, pool word of element 0} of this test
     // thread-parallel (kTP)
     uint32_t csh;            // shared address of memory cell 0 of the instance
     uint32_t cstr;           // bytes from one cell to the next
@@ -1160,7 +1160,8 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
             w = static_cast<uint32_t>(eff);
         } else {
             const uint32_t prm = p.y & 0x3F;
-            const uint32_t info = __ldg(L.binfo + prm);
+            const uint2 bi = __ldg(L.binfo + prm);
+            const uint32_t info = bi.x;
             if (eff < 0 || eff >= static_cast<int32_t>(info >> 8))
                 return L.trap(GEVO_TRAP_GLOBAL_OOB);
             const uint32_t elem = info & 0xFF;
@@ -1168,8 +1169,8 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
                 if (elem != f_aux(r))
                     return L.trap(GEVO_TRAP_GLOBAL_LOAD_TYPE);
                 if (!((L.writable >> prm) & 1ull))
-                    return L.set(f_res(r), __ldg(A.pool + A.pool_off[prm] +
-                                                 static_cast<size_t>(eff) * A.n_tests + L.t),
+                    return L.set(f_res(r), __ldg(A.pool + bi.y +
+                                                 static_cast<uint32_t>(eff) * static_cast<uint32_t>(A.n_tests)),
                                  elem);
             } else {
                 if (elem != val.y)
@@ -1233,7 +1234,8 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
         return true;
     }
     const uint32_t prm = p.y & 0x3F;
-    const uint32_t info = __ldg(L.binfo + prm);
+    const uint2 bi = __ldg(L.binfo + prm);
+    const uint32_t info = bi.x;
     if (eff < 0 || eff >= static_cast<int32_t>(info >> 8))
         return L.trap(GEVO_TRAP_GLOBAL_OOB);
     const uint32_t elem = info & 0xFF;
@@ -1243,7 +1245,7 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
             return L.trap(GEVO_TRAP_GLOBAL_LOAD_TYPE);
         const uint32_t w =
             priv ? A.priv[A.priv_off[prm] + static_cast<size_t>(eff) * A.n_inst + L.il]
-                 : __ldg(A.pool + A.pool_off[prm] + static_cast<size_t>(eff) * A.n_tests + L.t);
+                 : __ldg(A.pool + bi.y + static_cast<size_t>(eff) * A.n_tests);
         return L.set(f_res(r), w, elem);
     }
     if (elem != val.y)

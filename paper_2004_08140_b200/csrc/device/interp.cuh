@@ -37,7 +37,7 @@ struct InterpArgs {
     const uint32_t* param_payload; // [test][param]
     const int32_t* buf_size;       // [test][param]
     const uint8_t* buf_elem;       // [test][param]
-    const uint32_t* buf_info;      // [test][param] size << 8 | elem
+    const uint2* buf_info;         // [test][param] {size << 8 | elem, pool word of element 0}
     const uint8_t* setup_code;     // [test]
     const int32_t* setup_aux;      // [test]
     const uint32_t* pool;          // inputs + oracles, [row][test] blocks

@@ -156,9 +156,17 @@ DeviceSuite::DeviceSuite(Device& dev, SuiteImage image)
     upload(d.param_payload, image_.param_payload, s);
     upload(d.buf_size, image_.buf_size, s);
     upload(d.buf_elem, image_.buf_elem, s);
-    std::vector<uint32_t> info(image_.buf_size.size());
-    for (size_t i = 0; i < info.size(); ++i)
-        info[i] = (static_cast<uint32_t>(std::max(image_.buf_size[i], 0)) << 8) | image_.buf_elem[i];
+    // [test][param] {size << 8 | elem, word offset of the param's element 0 for
+    // this test in the interleaved pool}: one 8-byte load per global access
+    std::vector<uint32_t> info(image_.buf_size.size() * 2);
+    for (size_t i = 0; i < image_.buf_size.size(); ++i) {
+        const size_t t = i / std::max(image_.n_params, 1), p = i % std::max(image_.n_params, 1);
+        const uint64_t off = image_.pool_off[p] + t;
+        if (off > 0xFFFFFFFFull)
+            throw std::invalid_argument("test input pool exceeds 2^32 words");
+        info[2 * i] = (static_cast<uint32_t>(std::max(image_.buf_size[i], 0)) << 8) | image_.buf_elem[i];
+        info[2 * i + 1] = static_cast<uint32_t>(off);
+    }
     upload(d.buf_info, info, s);
     upload(d.setup_code, image_.setup_code, s);
     upload(d.setup_aux, image_.setup_aux, s);
@@ -203,7 +211,7 @@ gevo::InterpArgs base_args(DeviceSuite& suite, const ExecImage& ex, const EvalOp
     A.param_payload = d.param_payload.as<uint32_t>();
     A.buf_size = d.buf_size.as<int32_t>();
     A.buf_elem = d.buf_elem.as<uint8_t>();
-    A.buf_info = d.buf_info.as<uint32_t>();
+    A.buf_info = d.buf_info.as<uint2>();
     A.setup_code = d.setup_code.as<uint8_t>();
     A.setup_aux = d.setup_aux.as<int32_t>();
     A.pool = d.pool.as<uint32_t>();
