@@ -1181,9 +1181,9 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
             w = A.cell_off[prm] + static_cast<uint32_t>(eff);
         }
         if (op == GEVO_OP_LOAD) {
+            const uint2 x = L.cell_get(w);
             if (!L.seq)
                 tp_note(L, w, false);
-            const uint2 x = L.cell_get(w);
             if (p.y == GEVO_TAG_PTR_SHARED) {
                 const uint32_t wt = x.y & 0xFF;
                 if (wt == GEVO_TAG_UNDEF)
@@ -1197,7 +1197,6 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
             L.cell_put(w, val.x, val.y);
             return true;
         }
-        tp_note(L, w, true);
         // Same-phase stores of several simulated threads: the highest thread id
         // wins, and a thread's own stores land in program order (the
         // reference runs threads one after another, src/vm.cpp:121-142).
@@ -1205,6 +1204,7 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
         const uint32_t meta = val.y | (me << 8) | (L.epoch << 16);
         const unsigned long long want = (static_cast<unsigned long long>(meta) << 32) | val.x;
         const uint2 c0 = L.cell_get(w);
+        tp_note(L, w, true);
         unsigned long long cur = (static_cast<unsigned long long>(c0.y) << 32) | c0.x;
         for (;;) {
             const uint32_t m = static_cast<uint32_t>(cur >> 32);
@@ -1347,6 +1347,11 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
             // (another opcode, a division, a tag mismatch, a missing result
             // slot), which the general dispatch below then executes.
             for (;;) {
+#ifndef GEVO_RUN_BRANCHY
+                // next record in flight while this one executes (the sentinel
+                // after every block keeps pc + 1 inside the variant)
+                const uint4 nx = __ldg(code + pc + 1);
+#endif
                 const uint2 x = L.V(f_a(r)), y = L.V(f_b(r));
                 const uint32_t otag = f_otag(r);
                 const uint32_t res = f_res(r);
@@ -1354,6 +1359,31 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
                     break;
                 const float fx = __uint_as_float(x.x), fy = __uint_as_float(y.x);
                 uint32_t v, vt = otag;
+#ifndef GEVO_RUN_BRANCHY
+                {
+                    // branch-free: every cheap result is computed and op selects
+                    // one; a compare's predicate is a mask over (lt, eq, gt)
+                    // plus an invert bit (ne = !eq, true when unordered)
+                    const uint32_t o3 = op & 3u; // add/fadd 0, sub/fsub 1, mul/fmul 2
+                    const uint32_t vi = selp(o3 == 0, x.x + y.x, selp(o3 == 1, x.x - y.x, x.x * y.x));
+                    const uint32_t vf = selp(o3 == 0, __float_as_uint(__fadd_rn(fx, fy)),
+                                             selp(o3 == 1, __float_as_uint(__fsub_rn(fx, fy)),
+                                                  __float_as_uint(__fmul_rn(fx, fy))));
+                    const bool icmp = op == GEVO_OP_ICMP;
+                    const int32_t sx = static_cast<int32_t>(x.x), sy = static_cast<int32_t>(y.x);
+                    const uint32_t ib = static_cast<uint32_t>(sx < sy) | (static_cast<uint32_t>(sx == sy) << 1) |
+                                        (static_cast<uint32_t>(sx > sy) << 2);
+                    const uint32_t fb = static_cast<uint32_t>(fx < fy) | (static_cast<uint32_t>(fx == fy) << 1) |
+                                        (static_cast<uint32_t>(fx > fy) << 2);
+                    const uint32_t bits = selp(icmp, ib, fb);
+                    // eq 0x2, ne 0x2|inv, lt 0x1, le 0x3, gt 0x4, ge 0x6 (cmp() order)
+                    const uint32_t m = (0x6431A2u >> (f_aux(r) * 4)) & 0xFu;
+                    const uint32_t c = static_cast<uint32_t>((bits & m) != 0) ^ (m >> 3);
+                    const bool is_cmp = op >= GEVO_OP_ICMP;
+                    v = selp(is_cmp, c, selp(op <= GEVO_OP_MUL, vi, vf));
+                    vt = selp(is_cmp, static_cast<uint32_t>(GEVO_TAG_BOOL), otag);
+                }
+#else
                 switch (op) {
                 case GEVO_OP_ADD: v = x.x + y.x; break;
                 case GEVO_OP_SUB: v = x.x - y.x; break;
@@ -1370,9 +1400,14 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
                     vt = GEVO_TAG_BOOL;
                     break;
                 }
+#endif
                 L.W(res, v, vt);
                 ++pc;
+#ifndef GEVO_RUN_BRANCHY
+                r = nx;
+#else
                 r = __ldg(code + pc);
+#endif
                 op = f_op(r);
                 if (op > GEVO_OP_FCMP || op == GEVO_OP_SDIV || op == GEVO_OP_FDIV)
                     break;
