@@ -222,15 +222,15 @@ int gevo_batch_create(gevo_suite* s, gevo_batch** out) {
 
 int gevo_batch_add_ir(gevo_batch* b, const char* kernel_ir) {
     return guard([&] {
+        b->resident.reset(); // first: it holds a host registration of the blob
         b->image->add(parse_kernel(kernel_ir));
-        b->resident.reset();
     });
 }
 
 int gevo_batch_add_patch(gevo_batch* b, const char* patch_json) {
     return guard([&] {
+        b->resident.reset(); // first: it holds a host registration of the blob
         b->image->add(apply_patch(b->suite->kernel, patch_from_json(patch_json)).kernel);
-        b->resident.reset();
     });
 }
 

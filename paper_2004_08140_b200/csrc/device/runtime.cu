@@ -624,7 +624,13 @@ struct ResidentBatch {
     int launches = 0;
     uint64_t h2d = 0; // bytes uploaded by the evaluation in flight
     bool pending = false;
+    // the batch's host bytecode, page-locked in place so an uploading
+    // evaluation DMAs it directly (no staging copy on the host)
+    const void* reg = nullptr;
+    size_t reg_size = 0;
     ~ResidentBatch() {
+        if (reg)
+            cudaHostUnregister(const_cast<void*>(reg));
         if (stream)
             cudaStreamDestroy(stream);
         if (origin)
@@ -647,6 +653,15 @@ std::shared_ptr<ResidentBatch> make_resident(DeviceSuite& suite, BatchImage& bat
     rb->writable = writable_union(batch);
     rb->blob.reserve(blob.size() + 64);
     check(cudaMemcpy(rb->blob.ptr, blob.data(), blob.size(), cudaMemcpyHostToDevice), "resident");
+    if (!blob.empty()) {
+        if (cudaHostRegister(const_cast<uint8_t*>(blob.data()), blob.size(), cudaHostRegisterDefault) ==
+            cudaSuccess) {
+            rb->reg = blob.data();
+            rb->reg_size = blob.size();
+        } else {
+            cudaGetLastError(); // not page-lockable here: uploads go through the staging copy
+        }
+    }
     return rb;
 }
 
@@ -671,10 +686,13 @@ void evaluate_resident_async(ResidentBatch& rb, const ExecImage& exec, const Eva
     rb.h2d = upload ? upload->size() : 0;
     if (upload) {
         // host bytecode of the batch, copied in this evaluation (end-to-end form)
-        rb.h_blob.reserve(upload->size());
-        std::memcpy(rb.h_blob.ptr, upload->data(), upload->size());
-        check(cudaMemcpyAsync(rb.blob.ptr, rb.h_blob.ptr, upload->size(), cudaMemcpyHostToDevice,
-                              rb.stream),
+        const void* src = upload->data();
+        if (src != rb.reg || upload->size() != rb.reg_size) {
+            rb.h_blob.reserve(upload->size());
+            std::memcpy(rb.h_blob.ptr, upload->data(), upload->size());
+            src = rb.h_blob.ptr;
+        }
+        check(cudaMemcpyAsync(rb.blob.ptr, src, upload->size(), cudaMemcpyHostToDevice, rb.stream),
               "blob H2D");
     }
     gevo::InterpArgs A = base_args(*rb.suite, exec, opt);
