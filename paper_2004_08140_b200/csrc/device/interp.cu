@@ -2297,11 +2297,14 @@ __global__ void block_cost_kernel(const gevo_variant* __restrict__ variants,
                                   const gevo_inst* __restrict__ insts, uint32_t n_variants,
                                   const CostTableArg ct, uint4* __restrict__ out,
                                   int64_t* __restrict__ suffix) {
-    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    // one warp per variant, one lane per block: each lane sums its block's
+    // instruction classes back to front (the suffix costs refund() reads)
+    const uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
     if (v >= n_variants)
         return;
     const gevo_variant var = variants[v];
-    for (uint32_t b = 0; b < var.n_blocks; ++b) {
+    for (uint32_t b = lane; b < var.n_blocks; b += 32) {
         const gevo_block g = blocks[var.block_base + b];
         int64_t c = 0;
         for (uint32_t j = g.len; j-- > 0;) {
@@ -2416,7 +2419,7 @@ cudaError_t launch_block_cost(const gevo_block* blocks, const gevo_inst* insts,
     CostTableArg ct;
     for (int i = 0; i < GEVO_COST_CLASSES; ++i)
         ct.c[i] = cost_table[i];
-    block_cost_kernel<<<(n_variants + 127) / 128, 128, 0, stream>>>(variants, blocks, insts,
+    block_cost_kernel<<<(n_variants + 3) / 4, 128, 0, stream>>>(variants, blocks, insts,
                                                                     n_variants, ct, out, suffix);
     return cudaGetLastError();
 }
