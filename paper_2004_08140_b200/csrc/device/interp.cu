@@ -2319,41 +2319,81 @@ __global__ void block_cost_kernel(const gevo_variant* __restrict__ variants,
     }
 }
 
-// evaluate_fitness reduction (src/vm.cpp:558-579), one thread per variant,
-// tests in order so the double sum and the first failure match the reference.
+// evaluate_fitness reduction (src/vm.cpp:558-579): one warp per variant,
+// lane = test (chunks of 32). The first failing test comes from a ballot;
+// dynamic IR is an exact integer sum; the error maximum uses the reference's
+// comparison per element first (a NaN error never becomes the maximum, as in
+// the in-order loop) and is order-free after that; the cost mean divides the
+// in-order double sum of integer costs, which is exact -- hence equal to the
+// int64 sum -- while every partial sum stays below 2^53 (checked; otherwise
+// lane 0 adds in test order).
 __global__ void fitness_kernel(const gevo_test_record* __restrict__ rec, uint32_t n_variants,
                                int32_t n_tests, double tolerance,
                                gevo_variant_record* __restrict__ out) {
-    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t v = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int32_t lane = static_cast<int32_t>(threadIdx.x & 31);
     if (v >= n_variants)
         return;
     gevo_variant_record r{};
     r.failing_test = -1;
     r.accepted = 1;
     r.code = GEVO_OK;
-    double total = 0.0, worst = 0.0;
-    for (int32_t t = 0; t < n_tests; ++t) {
-        const gevo_test_record x = rec[static_cast<size_t>(v) * n_tests + t];
-        r.execs_ref += 1;
-        r.ir_ref += x.ir;
-        if (x.status != GEVO_STATUS_COMPLETED) {
+    int64_t ir = 0, cost = 0, execs = 0;
+    double worst = 0.0;
+    bool exact = true;
+    const gevo_test_record* vr = rec + static_cast<size_t>(v) * n_tests;
+    for (int32_t base = 0; base < n_tests; base += 32) {
+        const int32_t t = base + lane;
+        const bool have = t < n_tests;
+        gevo_test_record x{};
+        if (have)
+            x = vr[t];
+        const bool fail = have && (x.status != GEVO_STATUS_COMPLETED || x.error > tolerance);
+        const unsigned fm = __ballot_sync(0xffffffffu, fail);
+        const int32_t first = fm ? __ffs(fm) - 1 : 32;
+        const bool counted = have && lane <= first; // executed by the reference
+        const bool passed = have && lane < first;
+        int64_t c_ir = counted ? x.ir : 0, c_cost = passed ? x.cost : 0;
+        double w = passed ? ((0.0 < x.error) ? x.error : 0.0) : 0.0;
+        exact &= !passed || (x.cost >= 0 && x.cost < (int64_t(1) << 52));
+        for (int o = 16; o; o >>= 1) {
+            c_ir += __shfl_xor_sync(0xffffffffu, c_ir, o);
+            c_cost += __shfl_xor_sync(0xffffffffu, c_cost, o);
+            const double wo = __shfl_xor_sync(0xffffffffu, w, o);
+            w = (w < wo) ? wo : w;
+        }
+        ir += c_ir;
+        cost += c_cost;
+        execs += min(first + 1, n_tests - base);
+        worst = (worst < w) ? w : worst;
+        if (fm) {
+            const int32_t ft = base + first;
+            const gevo_test_record y = vr[ft];
             r.accepted = 0;
-            r.failing_test = t;
-            r.code = x.code;
-            r.aux = x.aux;
+            r.failing_test = ft;
+            if (y.status != GEVO_STATUS_COMPLETED) {
+                r.code = y.code;
+                r.aux = y.aux;
+            } else {
+                r.code = GEVO_FAIL_TOLERANCE;
+                r.fail_error = y.error;
+            }
             break;
         }
-        if (x.error > tolerance) {
-            r.accepted = 0;
-            r.failing_test = t;
-            r.code = GEVO_FAIL_TOLERANCE;
-            r.fail_error = x.error;
-            break;
-        }
-        worst = (worst < x.error) ? x.error : worst;
-        total = __dadd_rn(total, static_cast<double>(x.cost));
     }
+    exact = __all_sync(0xffffffffu, exact) && cost < (int64_t(1) << 53);
+    if (lane != 0)
+        return;
+    r.execs_ref = execs;
+    r.ir_ref = ir;
     if (r.accepted) {
+        double total = 0.0;
+        if (exact) {
+            total = static_cast<double>(cost);
+        } else {
+            for (int32_t t = 0; t < n_tests; ++t)
+                total = __dadd_rn(total, static_cast<double>(vr[t].cost));
+        }
         r.cost_mean = __ddiv_rn(total, static_cast<double>(n_tests));
         r.error_max = worst;
     }
@@ -2509,7 +2549,7 @@ cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream) {
 
 cudaError_t launch_fitness(const gevo_test_record* rec, uint32_t n_variants, int32_t n_tests,
                            double tolerance, gevo_variant_record* out, cudaStream_t stream) {
-    const unsigned grid = (n_variants + 127) / 128;
+    const unsigned grid = (n_variants + 3) / 4;
     if (grid == 0)
         return cudaSuccess;
     fitness_kernel<<<grid, 128, 0, stream>>>(rec, n_variants, n_tests, tolerance, out);
