@@ -1914,7 +1914,12 @@ __device__ __forceinline__ void tp_reset_thread(Lane<kM>& L, Thread& th) {
 } // namespace
 
 template <int kM>
-__global__ void __launch_bounds__(kTpMaxBlock, 1) interp_tp_kernel(const __grid_constant__ InterpArgs A) {
+#ifdef GEVO_TP_MAXNREG // register cap (occupancy experiments)
+#define GEVO_TP_BOUNDS __maxnreg__(GEVO_TP_MAXNREG)
+#else
+#define GEVO_TP_BOUNDS __launch_bounds__(kTpMaxBlock, 1)
+#endif
+__global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpArgs A) {
     constexpr bool kGC = kM == 3; // instance memory in global cells
     __shared__ TpInst S;
     TpGeom G;
@@ -2531,6 +2536,14 @@ cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream) {
     if (s.warps_per_cta == 0 || s.lanes != A.tp_lanes)
         return cudaErrorInvalidConfiguration;
     const unsigned grid = A.n_var * ((static_cast<uint32_t>(A.n_tests) + s.lanes - 1) / s.lanes);
+    static const int carveout = [] {
+        const char* e = std::getenv("GEVO_TP_CARVEOUT"); // shared-memory carveout % (tuning)
+        return e ? std::atoi(e) : -1;
+    }();
+    if (carveout >= 0) {
+        cudaFuncSetAttribute(interp_tp_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+        cudaFuncSetAttribute(interp_tp_kernel<3>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+    }
     if (gc) {
         const cudaError_t e = cudaFuncSetAttribute(
             interp_tp_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s.smem));
