@@ -1320,7 +1320,7 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
 #endif
     for (;;) {
 #ifdef GEVO_PREFETCH
-        const uint4 r = nxt;
+        uint4 r = nxt;
         nxt = __ldg(code + pc + 1);
 #else
         // (a one-ahead prefetch measured slower: the loop-carried copy of the
@@ -1412,6 +1412,9 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
                 if (op > GEVO_OP_FCMP || op == GEVO_OP_SDIV || op == GEVO_OP_FDIV)
                     break;
             }
+#ifdef GEVO_PREFETCH
+            nxt = __ldg(code + pc + 1);
+#endif
         }
 #endif
         bool ok;
