@@ -18,13 +18,18 @@
 #include "runtime.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <exception>
 #include <functional>
 #include <limits>
 #include <mutex>
 #include <thread>
+
+#include <unistd.h>
 
 namespace evoir {
 
@@ -39,41 +44,127 @@ enum StreamPurpose : uint64_t {
     kStreamMutate = 6,
 };
 
+// Persistent host worker pool. A search issues a few hundred parallel
+// sections (draw/apply/validate waves, encoding); spawning threads for each
+// would cost ~10^4 thread creations per run.
+class HostPool {
+public:
+    static HostPool& get() {
+        static HostPool p;
+        return p;
+    }
+    // fn(i) for i in [0, n) on the caller plus up to jobs - 1 workers; the
+    // first exception is rethrown after every participant stopped.
+    void run(size_t n, int jobs, const std::function<void(size_t)>& fn) {
+        std::unique_lock<std::mutex> section(section_mu_); // one section at a time
+        Job job;
+        job.fn = &fn;
+        job.n = n;
+        const int helpers = static_cast<int>(std::min<size_t>(
+            {static_cast<size_t>(std::max(jobs - 1, 0)), workers_.size(), n - 1}));
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            job_ = &job;
+            job.pending = helpers;
+            job.seats = helpers;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work(job);
+        std::unique_lock<std::mutex> g(mu_);
+        done_cv_.wait(g, [&] { return job.pending == 0; });
+        job_ = nullptr;
+        g.unlock();
+        if (job.err)
+            std::rethrow_exception(job.err);
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            quit_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_)
+            t.join();
+    }
+    static bool on_worker() { return worker_flag(); }
+    // a forked child inherits the pool object but not its threads
+    bool usable() const { return ::getpid() == pid_; }
+
+private:
+    struct Job {
+        const std::function<void(size_t)>* fn = nullptr;
+        size_t n = 0;
+        std::atomic<size_t> next{0};
+        std::atomic<bool> stop{false};
+        int pending = 0; // helpers still to finish (under mu_)
+        int seats = 0;   // helpers still to join (under mu_)
+        std::exception_ptr err;
+        std::mutex err_mu;
+    };
+    static bool& worker_flag() {
+        static thread_local bool f = false;
+        return f;
+    }
+    HostPool() : pid_(::getpid()) {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        for (unsigned w = 0; w + 1 < hw; ++w)
+            workers_.emplace_back([this] { loop(); });
+    }
+    static void work(Job& job) {
+        for (;;) {
+            const size_t i = job.next.fetch_add(1);
+            if (i >= job.n || job.stop.load())
+                return;
+            try {
+                (*job.fn)(i);
+            } catch (...) {
+                std::lock_guard<std::mutex> g(job.err_mu);
+                if (!job.err)
+                    job.err = std::current_exception();
+                job.stop.store(true);
+                return;
+            }
+        }
+    }
+    void loop() {
+        worker_flag() = true;
+        uint64_t seen = 0;
+        for (;;) {
+            Job* job = nullptr;
+            {
+                std::unique_lock<std::mutex> g(mu_);
+                cv_.wait(g, [&] { return quit_ || (gen_ != seen && job_ && job_->seats > 0); });
+                if (quit_)
+                    return;
+                seen = gen_;
+                job = job_;
+                --job->seats;
+            }
+            work(*job);
+            std::lock_guard<std::mutex> g(mu_);
+            if (--job->pending == 0)
+                done_cv_.notify_all();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex section_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    Job* job_ = nullptr;
+    uint64_t gen_ = 0;
+    bool quit_ = false;
+    pid_t pid_;
+};
+
 // Work-sharing loop over [0, n) on up to `jobs` host threads; the first
 // exception is rethrown after all workers stop.
 void host_parallel(size_t n, int jobs, const std::function<void(size_t)>& fn) {
-    if (jobs <= 1 || n <= 1) {
+    if (jobs <= 1 || n <= 1 || HostPool::on_worker() || !HostPool::get().usable()) {
         for (size_t i = 0; i < n; ++i)
             fn(i);
         return;
     }
-    std::atomic<size_t> next{0};
-    std::atomic<bool> stop{false};
-    std::exception_ptr err;
-    std::mutex mu;
-    std::vector<std::thread> ws;
-    const size_t nw = std::min<size_t>(static_cast<size_t>(jobs), n);
-    for (size_t w = 0; w < nw; ++w)
-        ws.emplace_back([&] {
-            for (;;) {
-                const size_t i = next.fetch_add(1);
-                if (i >= n || stop.load())
-                    return;
-                try {
-                    fn(i);
-                } catch (...) {
-                    std::lock_guard<std::mutex> g(mu);
-                    if (!err)
-                        err = std::current_exception();
-                    stop.store(true);
-                    return;
-                }
-            }
-        });
-    for (auto& t : ws)
-        t.join();
-    if (err)
-        std::rethrow_exception(err);
+    HostPool::get().run(n, jobs, fn);
 }
 
 b200::Collective& collective_slot() {
@@ -84,6 +175,20 @@ b200::Collective& collective_slot() {
 double ms_since(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
+
+// GEVO_TRACE=1: wall-time split of a search on stderr (diagnostic)
+struct Trace {
+    double verdicts_ms = 0, eval_ms = 0;
+    double select_ms = 0, cx_ms = 0, mut_ms = 0, rank_ms = 0, archive_ms = 0;
+    static Trace& get() {
+        static Trace t;
+        return t;
+    }
+    static bool on() {
+        static const bool v = std::getenv("GEVO_TRACE") != nullptr;
+        return v;
+    }
+};
 
 // Wave schedule: attempts drawn per slot per round before the next device batch.
 int wave_size(int used, int retries) {
@@ -100,6 +205,10 @@ std::vector<EvalOutcome> device_verdicts(b200::DeviceSuite& suite, const b200::E
     std::vector<EvalOutcome> out(ks.size());
     if (ks.empty())
         return out;
+    struct Timer {
+        std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+        ~Timer() { Trace::get().verdicts_ms += ms_since(t0); }
+    } timer;
     if (suite.image().n_tests == 0) {
         for (auto& o : out)
             o = EvalOutcome::rejected(-1, "no test cases");
@@ -140,8 +249,10 @@ std::vector<EvalOutcome> device_verdicts(b200::DeviceSuite& suite, const b200::E
     opt.tolerance = tol;
     opt.early_exit = true;
     b200::EvalResult r;
+    const auto t_ev = std::chrono::steady_clock::now();
     if (hi > lo)
         r = b200::evaluate(suite, batch, ex, opt);
+    Trace::get().eval_ms += ms_since(t_ev);
     std::vector<gevo_variant_record> recs;
     if (shard) {
         const size_t m = (n + W - 1) / W;
@@ -528,6 +639,12 @@ void Engine::step_generation() {
     const size_t pop = static_cast<size_t>(cfg_.pop_size);
     const uint64_t gen = static_cast<uint64_t>(generation_) + 1;
 
+    auto tp = std::chrono::steady_clock::now();
+    auto lap = [&](double& acc) {
+        acc += ms_since(tp);
+        tp = std::chrono::steady_clock::now();
+    };
+    Trace& tr = Trace::get();
     Rng trng = Rng::stream(cfg_.master_seed, gen, 0, kStreamTournament);
     const std::vector<int> off_idx = tournament_select(rank_, population_.size(), pop, trng);
     const std::vector<int> elite_idx = select_best(rank_, pop / 4);
@@ -548,6 +665,7 @@ void Engine::step_generation() {
     for (auto& f : mut_fire)
         f = gm.chance(cfg_.mutate_rate) ? 1 : 0;
 
+    lap(tr.select_ms);
     // Crossover: every firing pair is one speculative job.
     std::vector<OperatorStats> pair_stats(pop / 2);
     {
@@ -572,6 +690,7 @@ void Engine::step_generation() {
             offspring[2 * pairs[i] + 1] = std::move(jobs[i].rb);
         }
     }
+    lap(tr.cx_ms);
     // Mutation: every firing slot is one speculative job.
     std::vector<OperatorStats> mut_stats(pop);
     {
@@ -597,6 +716,7 @@ void Engine::step_generation() {
             offspring[slots[i]] = std::move(jobs[i].result);
     }
 
+    lap(tr.mut_ms);
     OperatorStats gen_stats;
     for (const auto& s : pair_stats)
         gen_stats.merge(s);
@@ -618,8 +738,10 @@ void Engine::step_generation() {
     for (int i : keep)
         next.push_back(std::move(pool[static_cast<size_t>(i)]));
     population_ = std::move(next);
+    lap(tr.rank_ms);
     for (const auto& ind : population_)
         archive_add(ind);
+    lap(tr.archive_ms);
     rank_current();
     ++generation_;
     log_generation(gen_stats);
@@ -679,6 +801,8 @@ void Engine::log_generation(const OperatorStats& gs) {
 }
 
 SearchResult Engine::run(const std::vector<TestCase>& heldout) {
+    const auto t_run = std::chrono::steady_clock::now();
+    Trace::get() = Trace{};
     initialize_population();
     if (cfg_.budget.kind == Budget::Kind::Generations) {
         for (int g = 0; g < cfg_.budget.generations; ++g)
@@ -705,6 +829,16 @@ SearchResult Engine::run(const std::vector<TestCase>& heldout) {
             }
         }
     }
+    if (Trace::on())
+        std::fprintf(stderr,
+                     "[gevo trace] run %.1f ms: verdicts %.1f (encode+gen %.1f, evaluate %.1f, "
+                     "device %.1f), other host %.1f; select %.1f cx %.1f mut %.1f rank %.1f "
+                     "archive %.1f (archive size %zu)\n",
+                     ms_since(t_run), Trace::get().verdicts_ms, counters_.host_gen_ms,
+                     Trace::get().eval_ms, counters_.device_ms,
+                     ms_since(t_run) - Trace::get().verdicts_ms, Trace::get().select_ms,
+                     Trace::get().cx_ms, Trace::get().mut_ms, Trace::get().rank_ms,
+                     Trace::get().archive_ms, archive_.size());
     SearchResult r;
     r.population = population_;
     r.archive = archive_;
