@@ -180,6 +180,7 @@ double ms_since(std::chrono::steady_clock::time_point t0) {
 struct Trace {
     double verdicts_ms = 0, eval_ms = 0;
     double select_ms = 0, cx_ms = 0, mut_ms = 0, rank_ms = 0, archive_ms = 0;
+    double cx_gen_ms = 0, cx_resolve_ms = 0, mut_gen_ms = 0, mut_resolve_ms = 0;
     static Trace& get() {
         static Trace t;
         return t;
@@ -439,8 +440,10 @@ void Engine::run_mutations(std::vector<MutJob>& jobs) const {
                     ks.push_back(&at.kernel);
                 }
         counters_.host_gen_ms += ms_since(t0);
+        Trace::get().mut_gen_ms += ms_since(t0);
         const auto verdicts =
             device_verdicts(*suite_, *exec_img_, ks, cfg_.tolerance, false, counters_, cfg_.jobs);
+        const auto t_res = std::chrono::steady_clock::now();
         // 3. resolve each slot in attempt order
         for (MutJob* j : active) {
             for (auto& at : j->wave) {
@@ -466,8 +469,9 @@ void Engine::run_mutations(std::vector<MutJob>& jobs) const {
                 j->result = *j->parent;
                 j->done = true;
             }
-            j->wave.clear();
         }
+        host_parallel(active.size(), cfg_.jobs, [&](size_t i) { active[i]->wave.clear(); });
+        Trace::get().mut_resolve_ms += ms_since(t_res);
     }
 }
 
@@ -520,8 +524,10 @@ void Engine::run_crossovers(std::vector<CxJob>& jobs) const {
                 }
             }
         counters_.host_gen_ms += ms_since(t0);
+        Trace::get().cx_gen_ms += ms_since(t0);
         const auto verdicts =
             device_verdicts(*suite_, *exec_img_, ks, cfg_.tolerance, false, counters_, cfg_.jobs);
+        const auto t_res = std::chrono::steady_clock::now();
         for (CxJob* j : active) {
             for (auto& at : j->wave) {
                 ++j->used;
@@ -547,8 +553,10 @@ void Engine::run_crossovers(std::vector<CxJob>& jobs) const {
                 j->rb = *j->b;
                 j->done = true;
             }
-            j->wave.clear();
         }
+        // the losing attempts' kernels are freed on the worker threads
+        host_parallel(active.size(), cfg_.jobs, [&](size_t i) { active[i]->wave.clear(); });
+        Trace::get().cx_resolve_ms += ms_since(t_res);
     }
 }
 
@@ -833,12 +841,14 @@ SearchResult Engine::run(const std::vector<TestCase>& heldout) {
         std::fprintf(stderr,
                      "[gevo trace] run %.1f ms: verdicts %.1f (encode+gen %.1f, evaluate %.1f, "
                      "device %.1f), other host %.1f; select %.1f cx %.1f mut %.1f rank %.1f "
-                     "archive %.1f (archive size %zu)\n",
+                     "archive %.1f (archive size %zu); cx gen %.1f resolve %.1f, mut gen %.1f "
+                     "resolve %.1f\n",
                      ms_since(t_run), Trace::get().verdicts_ms, counters_.host_gen_ms,
                      Trace::get().eval_ms, counters_.device_ms,
                      ms_since(t_run) - Trace::get().verdicts_ms, Trace::get().select_ms,
                      Trace::get().cx_ms, Trace::get().mut_ms, Trace::get().rank_ms,
-                     Trace::get().archive_ms, archive_.size());
+                     Trace::get().archive_ms, archive_.size(), Trace::get().cx_gen_ms,
+                     Trace::get().cx_resolve_ms, Trace::get().mut_gen_ms, Trace::get().mut_resolve_ms);
     SearchResult r;
     r.population = population_;
     r.archive = archive_;
