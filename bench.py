@@ -73,7 +73,7 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", "1")))
 
 
-def workload_config(args, world):
+def workload_config(args, world, backend="nccl"):
     return {
         "workload": "config2: GEVO candidate batches, Rodinia-style IR kernels "
                     "hot-branch/nw-sync/bfs-load, %d validated mutants per kernel x %d "
@@ -84,7 +84,8 @@ def workload_config(args, world):
         "tests": args.tests,
         "budget": 1_000_000,
         "tolerance": 0.0,
-        "parallelism": "population-sharded dp%d (fitness records all-gathered over NCCL)" % world,
+        "parallelism": "population-sharded dp%d (fitness records all-gathered over %s)" %
+                       (world, "NCCL" if backend == "nccl" else backend),
         "l2": "flushed between timed steps (512 MiB write)",
     }
 
@@ -212,13 +213,15 @@ def b200_arm(args):
     rank, local, world = dist_env()
     # one process per GPU; more ranks than GPUs (a functional check of the
     # N > 1 path on a smaller box) share devices round-robin
+    shared = world > torch.cuda.device_count()
     local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     os.environ["GEVO_DEVICE"] = str(local)
-    coll_dev = "cuda" if os.environ.get("BENCH_DIST_BACKEND", "nccl") == "nccl" else "cpu"
+    # NCCL needs a distinct GPU per rank: ranks sharing a device exchange over gloo
+    backend = os.environ.get("BENCH_DIST_BACKEND", "gloo" if shared else "nccl")
+    coll_dev = "cuda" if backend == "nccl" else "cpu"
     if world > 1:
         import torch.distributed as dist
-        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -421,7 +424,7 @@ def b200_arm(args):
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "i32/f32 (IEEE, no FMA) + f64 error",
         "data": "synthetic (seeded generate_tests inputs, seeded mutant walks)",
-        "config": workload_config(args, world),
+        "config": workload_config(args, world, backend),
         "ir_per_s": ref_ir_step * args.steps * world / (dev_ms / 1000.0),
         "executions_per_step": ref_execs_step * world,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
