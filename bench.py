@@ -271,10 +271,14 @@ def b200_arm(args):
     timed_launches = [0]
     kernel_ms = {k: [] for k in KERNELS}
 
+    # launch order of the concurrent batches (records are still gathered in
+    # KERNELS order)
+    order = os.environ.get("BENCH_LAUNCH_ORDER", ",".join(KERNELS)).split(",")
+
     def step_resident():
         # the three batches are independent: each runs on its own stream and
         # their launches (and launch tails) overlap on the GPU
-        for k in KERNELS:
+        for k in order:
             batches[k].eval_resident_async(cfgs[k], tolerance=0.0, early_exit=True)
         recs = []
         for k in KERNELS:
@@ -312,7 +316,7 @@ def b200_arm(args):
 
     # e2e through the C ABI with host bytecode (H2D + kernels + D2H records)
     def step_e2e():
-        for k in KERNELS:
+        for k in order:
             batches[k].eval_resident_async(cfgs[k], tolerance=0.0, early_exit=True, upload=True)
         return [batches[k].wait(records=True)[1] for k in KERNELS]
 
