@@ -1862,12 +1862,14 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
 namespace {
 
 enum : uint32_t { kInstPar = 0, kInstSeq = 1, kInstDone = 2 };
+constexpr uint32_t kStickySeq = 2;
 enum : uint32_t { kActContinue = 0, kActFinish = 1, kActRestart = 2, kActNone = 3 };
 
 struct TpInst {
     int32_t min_stop[32];
     uint32_t state[32];
     uint32_t conflict[32];
+    uint32_t nconf[32]; // phases of the instance re-run after a conflict
     uint32_t status[32];
     uint32_t code[32];
     int32_t aux[32];
@@ -2012,6 +2014,7 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
         S.cost[c] = 0;
         S.ir[c] = 0;
         S.jumps[c] = 0;
+        S.nconf[c] = 0;
         S.aux[c] = 0;
         S.code[c] = GEVO_OK;
         if (c >= Ln || tc >= nt) {
@@ -2199,8 +2202,10 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
                 L.code_out = GEVO_OK;
                 L.aux = 0;
             }
-            if (leader)
+            if (leader) {
                 S.state[j] = kInstSeq;
+                ++S.nconf[j];
+            }
         } else if (act == kActFinish) {
             const bool mine = ts >= T || tid <= ts;
             atomicAdd(S.cost + j, static_cast<unsigned long long>(mine ? L.cost : cost_commit));
@@ -2225,11 +2230,15 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
             cost_commit = L.cost;
             ir_commit = L.ir;
             // the next phase runs concurrently again (a single-phase variant
-            // never continues; a re-run phase 0 has no snapshot to return to)
+            // never continues; a re-run phase 0 has no snapshot to return to),
+            // unless the instance keeps conflicting: after kStickySeq re-runs
+            // its remaining phases go straight to thread-id order (typically a
+            // barrier inside a loop whose every iteration conflicts), saving
+            // the discarded concurrent attempt and its snapshot
             if (snap) {
                 first_phase = false;
                 if (leader)
-                    S.state[j] = kInstPar;
+                    S.state[j] = S.nconf[j] >= kStickySeq ? kInstSeq : kInstPar;
             }
         }
         if (__syncthreads_and(!active || S.state[j] == kInstDone))
