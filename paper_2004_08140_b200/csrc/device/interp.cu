@@ -1130,6 +1130,89 @@ __device__ __forceinline__ void tp_note(const Lane<kM>& L, uint32_t w, bool writ
     }
 }
 
+// Fast path of the common memory instructions of a thread-parallel lane: all
+// operands are fetched at once (independent shared-memory reads in flight
+// together) and the instruction completes here when every check passes. Any
+// failing check returns false before a side effect, and mem_op then runs the
+// instruction with the reference's check order and trap reasons.
+template <int kM>
+__device__ __forceinline__ bool mem_fast(const InterpArgs& A, Lane<kM>& L, const uint4 r) {
+    const uint32_t op = f_op(r), res = f_res(r);
+    const bool store = op == GEVO_OP_STORE;
+    const uint2 p = L.V(f_a(r)), ix = L.V(f_b(r));
+    const uint2 val = store ? L.V(f_c(r)) : make_uint2(0, 0);
+    if (ix.y != GEVO_TAG_I32)
+        return false;
+    if (store ? (val.y != GEVO_TAG_I32 && val.y != GEVO_TAG_F32) : res == GEVO_NO_RESULT)
+        return false;
+    const int64_t eff = static_cast<int64_t>(static_cast<int32_t>(p.x)) +
+                        static_cast<int64_t>(static_cast<int32_t>(ix.x));
+    uint32_t w;
+    if (p.y == GEVO_TAG_PTR_SHARED) {
+        if (static_cast<uint64_t>(eff) >= static_cast<uint64_t>(static_cast<uint32_t>(A.shared_words)))
+            return false;
+        w = static_cast<uint32_t>(eff);
+        if (!store) {
+            const uint2 x = L.cell_get(w);
+            const uint32_t wt = x.y & 0xFF;
+            if (wt != f_aux(r)) // uninitialised (tag 0) or another type
+                return false;
+            if (!L.seq)
+                tp_note(L, w, false);
+            L.W(res, x.x, wt);
+            return true;
+        }
+    } else if (p.y >= static_cast<uint32_t>(GEVO_TAG_PTR_GLOBAL)) {
+        const uint32_t prm = p.y & 0x3F;
+        const uint2 bi = __ldg(L.binfo + prm);
+        if (static_cast<uint64_t>(eff) >= static_cast<uint64_t>(bi.x >> 8))
+            return false;
+        const uint32_t elem = bi.x & 0xFF;
+        const bool priv = (L.writable >> prm) & 1ull;
+        if (!store) {
+            if (elem != f_aux(r))
+                return false;
+            if (!priv) {
+                L.W(res, __ldg(A.pool + bi.y + static_cast<uint32_t>(eff) * static_cast<uint32_t>(A.n_tests)),
+                    elem);
+                return true;
+            }
+            w = A.cell_off[prm] + static_cast<uint32_t>(eff);
+            const uint2 x = L.cell_get(w);
+            if (!L.seq)
+                tp_note(L, w, false);
+            L.W(res, x.x, x.y & 0xFF);
+            return true;
+        }
+        if (elem != val.y || !priv)
+            return false;
+        w = A.cell_off[prm] + static_cast<uint32_t>(eff);
+    } else {
+        return false;
+    }
+    // store to an instance cell (as mem_op)
+    if (L.seq) {
+        L.cell_put(w, val.x, val.y);
+        return true;
+    }
+    const uint32_t me = static_cast<uint32_t>(L.tid) + 1;
+    const uint32_t meta = val.y | (me << 8) | (L.epoch << 16);
+    const unsigned long long want = (static_cast<unsigned long long>(meta) << 32) | val.x;
+    const uint2 c0 = L.cell_get(w);
+    tp_note(L, w, true);
+    unsigned long long cur = (static_cast<unsigned long long>(c0.y) << 32) | c0.x;
+    for (;;) {
+        const uint32_t m = static_cast<uint32_t>(cur >> 32);
+        if ((m >> 16) == L.epoch && ((m >> 8) & 0xFF) > me)
+            break;
+        const unsigned long long prev = L.cell_cas(w, cur, want);
+        if (prev == cur)
+            break;
+        cur = prev;
+    }
+    return true;
+}
+
 // Memory instructions (vm.cpp:238-283, 447-460): off the hot dispatch path.
 template <int kM>
 __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const uint4 r) {
@@ -1554,7 +1637,11 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
 #endif
             continue;
         } else if (op == GEVO_OP_LOAD || op == GEVO_OP_STORE) {
+#ifndef GEVO_NO_MEM_FAST
+            ok = (Lane<kM>::kTP && mem_fast(A, L, r)) || mem_op(A, L, r);
+#else
             ok = mem_op(A, L, r);
+#endif
         } else if (op == GEVO_OP_SYNC || op == GEVO_OP_RET) {
             th.ip = static_cast<int32_t>(pc - b.start);
             refund(A, L, th, b, th.ip + 1);
