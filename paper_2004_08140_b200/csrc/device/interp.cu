@@ -979,6 +979,21 @@ __device__ __forceinline__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Th
         // <= 2 phis resolved for this edge at encode time (no arm matching)
         const uint32_t ref0 = edge.x & 0xFFFF;
         uint2 v0, v1;
+        if (n == 2) {
+            // both arms read at once; the checks below then only re-read
+            // on a failure path
+            const uint32_t ref1 = edge.y & 0xFFFF;
+            if (ref0 != GEVO_EDGE_NOINC && ref1 != GEVO_EDGE_NOINC) {
+                v0 = L.V(ref0);
+                v1 = L.V(ref1);
+                if (!bad_tag(v0.y) && !bad_tag(v1.y)) {
+                    th.ip = 2;
+                    L.W(edge.y >> 16, v1.x, v1.y);
+                    L.W(edge.x >> 16, v0.x, v0.y);
+                    return true;
+                }
+            }
+        }
         if (ref0 == GEVO_EDGE_NOINC) {
             refund(A, L, th, b, 1);
             return L.trap(GEVO_TRAP_PHI_NO_INCOMING);
@@ -1344,7 +1359,17 @@ template <int kM>
 __device__ __forceinline__ bool misc_op(const InterpArgs& A, Lane<kM>& L, const uint4 r) {
     switch (f_op(r)) {
     case GEVO_OP_SELECT: {
-        const uint2 c = L.V(f_a(r));
+        // both arms are read with the condition (independent shared reads in
+        // flight together); the common case completes here, anything else
+        // follows the reference order below (it fetches only the chosen arm)
+        const uint2 c = L.V(f_a(r)), vb = L.V(f_b(r)), vc = L.V(f_c(r));
+        if (c.y == GEVO_TAG_BOOL) {
+            const uint2 v = c.x ? vb : vc;
+            if (v.y == f_aux(r) && f_res(r) != GEVO_NO_RESULT && !bad_tag(v.y)) {
+                L.W(f_res(r), v.x, v.y);
+                return true;
+            }
+        }
         if (c.y != GEVO_TAG_BOOL)
             return L.scalar_fail(f_a(r), c.y);
         uint2 v;
@@ -1355,6 +1380,15 @@ __device__ __forceinline__ bool misc_op(const InterpArgs& A, Lane<kM>& L, const 
         return L.set(f_res(r), v.x, v.y);
     }
     case GEVO_OP_GETINDEX: {
+        {
+            const uint2 p = L.V(f_a(r)), ix = L.V(f_b(r));
+            if ((p.y == GEVO_TAG_PTR_SHARED || p.y >= static_cast<uint32_t>(GEVO_TAG_PTR_GLOBAL)) &&
+                (p.y == GEVO_TAG_PTR_SHARED ? 1u : 0u) == f_aux(r) && ix.y == GEVO_TAG_I32 &&
+                f_res(r) != GEVO_NO_RESULT) {
+                L.W(f_res(r), p.x + ix.x, p.y);
+                return true;
+            }
+        }
         uint2 p;
         if (!L.pointer(f_a(r), p))
             return false;
