@@ -2207,8 +2207,10 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
                 th_snap = th;
                 for (uint32_t x = 0; x < L.n_values; ++x)
                     A.tp_snap[static_cast<size_t>(x) * A.n_spin + L.sl] = L.V(x);
-                for (uint32_t x = tid; x < A.n_cells; x += T)
-                    sts2(back0 + (x * Ln + j) * 8, lds2(L.cell(x)).x, lds2(L.cell(x)).y);
+                for (uint32_t x = tid; x < A.n_cells; x += T) {
+                    const uint2 c = lds2(L.cell(x));
+                    sts2(back0 + (x * Ln + j) * 8, c.x, c.y);
+                }
             }
         }
         if (leader) {
