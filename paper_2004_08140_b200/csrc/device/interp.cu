@@ -2504,7 +2504,7 @@ __global__ void fitness_kernel(const gevo_test_record* __restrict__ rec, uint32_
         }
         ir += c_ir;
         cost += c_cost;
-        execs += min(first + 1, n_tests - base);
+        execs += fm ? first + 1 : min(32, n_tests - base);
         worst = (worst < w) ? w : worst;
         if (fm) {
             const int32_t ft = base + first;
