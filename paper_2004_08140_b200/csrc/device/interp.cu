@@ -210,7 +210,8 @@ struct Lane {
     uint32_t rsh, wsh;       // shared addresses of this lane's read / write bitset chunk 0
     uint32_t bstr;           // bytes from one bitset chunk to the next
     uint32_t msh;            // shared address of the instance's min_stop
-    uint32_t fsh;            // shared address of the instance's conflict flag (kGC)
+    uint32_t fsh;            // shared address of the instance's conflict flag
+    uint32_t tsh_star;       // shared address of the instance's lowest conflicting thread
     uint2* gcell;            // kGC: cell 0 of the instance ([word][instance] in global memory)
     unsigned long long* gshadow; // kGC: per-word same-phase reader / writer record
     uint32_t gstr;           // kGC: elements from one word to the next (instances per launch)
@@ -1174,6 +1175,7 @@ __device__ __forceinline__ bool mem_fast(const InterpArgs& A, Lane<kM>& L, const
                 return false;
             if (!L.seq)
                 tp_note(L, w, false);
+            tp_read_check(L, x.y);
             L.W(res, x.x, wt);
             return true;
         }
@@ -1196,6 +1198,7 @@ __device__ __forceinline__ bool mem_fast(const InterpArgs& A, Lane<kM>& L, const
             const uint2 x = L.cell_get(w);
             if (!L.seq)
                 tp_note(L, w, false);
+            tp_read_check(L, x.y);
             L.W(res, x.x, x.y & 0xFF);
             return true;
         }
@@ -1226,6 +1229,24 @@ __device__ __forceinline__ bool mem_fast(const InterpArgs& A, Lane<kM>& L, const
         cur = prev;
     }
     return true;
+}
+
+// A shared-memory-cell read of a concurrent phase that returned another
+// simulated thread's write of this phase (the cell's writer/epoch meta): the
+// reference, running threads one after another, could not have produced it
+// (a higher writer runs later; a lower one may still write again), so the
+// instance is flagged and the reading thread bounds the re-run's
+// conflict-free prefix. Reads of phase-start or own values are clean; whether
+// a lower thread writes such a word later is checked with the bitsets at the
+// phase end.
+template <int kM>
+__device__ __forceinline__ void tp_read_check(const Lane<kM>& L, uint32_t meta) {
+    if (Lane<kM>::kGC || L.seq)
+        return;
+    if ((meta >> 16) == (L.epoch & 0xFFFFu) && ((meta >> 8) & 0xFFu) != static_cast<uint32_t>(L.tid) + 1) {
+        sts1(L.fsh, 1u);
+        asm volatile("red.shared.min.s32 [%0], %1;" ::"r"(L.tsh_star), "r"(L.tid) : "memory");
+    }
 }
 
 // Memory instructions (vm.cpp:238-283, 447-460): off the hot dispatch path.
@@ -1282,6 +1303,7 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
             const uint2 x = L.cell_get(w);
             if (!L.seq)
                 tp_note(L, w, false);
+            tp_read_check(L, x.y);
             if (p.y == GEVO_TAG_PTR_SHARED) {
                 const uint32_t wt = x.y & 0xFF;
                 if (wt == GEVO_TAG_UNDEF)
@@ -1991,6 +2013,8 @@ struct TpInst {
     uint32_t state[32];
     uint32_t conflict[32];
     uint32_t nconf[32]; // phases of the instance re-run after a conflict
+    int32_t tstar[32];  // lowest thread whose reads overlapped another thread's writes
+    int32_t seqfrom[32];// re-run: threads below run concurrently, the rest in id order
     uint32_t status[32];
     uint32_t code[32];
     int32_t aux[32];
@@ -2111,6 +2135,7 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
     L.bstr = blockDim.x * 4;
     L.msh = smem_addr(S.min_stop + j);
     L.fsh = smem_addr(S.conflict + j);
+    L.tsh_star = smem_addr(S.tstar + j);
     const uint32_t il = vl * nt + t; // launch-local instance (global cells)
     L.gcell = kGC ? A.gcells + il : nullptr;
     L.gshadow = kGC ? A.gshadow + il : nullptr;
@@ -2136,6 +2161,7 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
         S.ir[c] = 0;
         S.jumps[c] = 0;
         S.nconf[c] = 0;
+        S.seqfrom[c] = 0;
         S.aux[c] = 0;
         S.code[c] = GEVO_OK;
         if (c >= Ln || tc >= nt) {
@@ -2216,6 +2242,7 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
         if (leader) {
             S.min_stop[j] = INT32_MAX;
             S.conflict[j] = 0;
+            S.tstar[j] = INT32_MAX;
         }
         __syncthreads();
         int kind = kStopIdle;
@@ -2225,8 +2252,14 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
         const bool any_seq = __syncthreads_or(st == kInstSeq);
         const uint32_t rounds = any_seq ? T + 1 : 1;
         for (uint32_t u = 0; u < rounds; ++u) {
-            const bool go = u == 0 ? st == kInstPar
+            // a re-run phase first repeats its conflict-free prefix (threads
+            // below seqfrom: none of them read a word another thread wrote, so
+            // concurrently they reproduce their reference results) and then
+            // runs the remaining threads one after another
+            const bool go = u == 0 ? (st == kInstPar ||
+                                      (st == kInstSeq && static_cast<int32_t>(tid) < S.seqfrom[j]))
                                    : (st == kInstSeq && tid == u - 1 &&
+                                      static_cast<int32_t>(tid) >= S.seqfrom[j] &&
                                       S.min_stop[j] == INT32_MAX);
             if (go) {
                 L.seq = u != 0;
@@ -2249,19 +2282,28 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
         }
         __syncthreads();
         if (!kGC && st == kInstPar) {
-            // same-phase cross-thread read/write: R_tid & W_u, u != tid
-            uint32_t hit = 0;
-            for (uint32_t k = 0; k < A.n_chunks && !hit; ++k) {
+            // Words this thread read that another thread wrote in the phase.
+            // Written by a LOWER thread: the reference shows that write, so
+            // the phase conflicts. Written only by higher threads: the reads
+            // saw phase-start values (a higher thread's write, had it been
+            // seen, was flagged by tp_read_check) -- no conflict, but the
+            // thread is then not part of a re-run's conflict-free prefix.
+            uint32_t lo = 0, hi = 0;
+            for (uint32_t k = 0; k < A.n_chunks && !lo; ++k) {
                 const uint32_t r = lds1(L.rsh + k * L.bstr);
                 if (!r)
                     continue;
                 const uint32_t wk = bits0 + (bit_words + k * blockDim.x) * 4;
-                for (uint32_t u = 0; u < T; ++u)
-                    if (u != tid)
-                        hit |= r & lds1(wk + G.lane_of(u, j) * 4);
+                for (uint32_t u = 0; u < T; ++u) {
+                    const uint32_t o = r & lds1(wk + G.lane_of(u, j) * 4);
+                    lo |= u < tid ? o : 0u;
+                    hi |= u > tid ? o : 0u;
+                }
             }
-            if (hit)
+            if (lo)
                 S.conflict[j] = 1;
+            if (lo | hi)
+                atomicMin(S.tstar + j, static_cast<int32_t>(tid));
         }
         __syncthreads();
         // Phase verdict of instance j (every thread of it derives the same one).
@@ -2328,6 +2370,15 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
             if (leader) {
                 S.state[j] = kInstSeq;
                 ++S.nconf[j];
+                // global-cell instances restart from their initial state (not
+                // the conflicting phase's start) and learn of conflicts at the
+                // access: fully in id order
+                // (and a multi-phase instance without a snapshot would restart
+                // from phase 0, where the prefix bound does not apply)
+                S.seqfrom[j] = (kGC || S.tstar[j] == INT32_MAX ||
+                                (!snap && (var.flags & GEVO_VAR_HAS_SYNC)))
+                                   ? 0
+                                   : S.tstar[j];
             }
         } else if (act == kActFinish) {
             const bool mine = ts >= T || tid <= ts;
@@ -2362,6 +2413,8 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
                 first_phase = false;
                 if (leader)
                     S.state[j] = S.nconf[j] >= kStickySeq ? kInstSeq : kInstPar;
+                if (leader)
+                    S.seqfrom[j] = 0;
             }
         }
         if (__syncthreads_and(!active || S.state[j] == kInstDone))
