@@ -440,7 +440,10 @@ __device__ __forceinline__ void spin_abandon(Spin& S, const Thread& th, Lane<kM>
                                              uint32_t why) {
     ++S.attempts;
     S.skip = S.attempts & 3u;
-    S.next = S.attempts > 12 ? INT64_MAX : th.executed + (th.executed >> 1) + 64;
+#ifndef GEVO_SPIN_BACKOFF
+#define GEVO_SPIN_BACKOFF 1 // next attempt after executed * (1 + 2^-shift): shift 1 = x1.5
+#endif
+    S.next = S.attempts > 12 ? INT64_MAX : th.executed + (th.executed >> GEVO_SPIN_BACKOFF) + 64;
     if (S.mode == 2 && S.K < S.H && S.attempts <= 12) {
         // The anchor's loop leaves its path within K + 1 iterations (an inner
         // loop running out): try again right after that, at a block other
