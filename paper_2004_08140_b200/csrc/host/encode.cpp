@@ -224,12 +224,44 @@ void BatchImage::add(const Kernel& k) {
         throw std::invalid_argument("too many blocks");
     const uint32_t P = static_cast<uint32_t>(suite_.n_params);
 
+    // Value ids are small non-negative integers in practice: flat tables
+    // indexed by id then (hash maps only for unusual ids).
+    int32_t id_lo = 0, id_hi = -1;
+    k.for_each_instruction([&](const BasicBlock&, const Instruction& in) {
+        if (in.result) {
+            id_lo = std::min(id_lo, *in.result);
+            id_hi = std::max(id_hi, *in.result);
+        }
+        for (const Operand& o : in.operands)
+            if (o.is_value()) {
+                id_lo = std::min(id_lo, o.value);
+                id_hi = std::max(id_hi, o.value);
+            }
+    });
+    const bool dense = id_lo >= 0 && id_hi < (1 << 20);
+    const size_t n_ids = dense ? static_cast<size_t>(id_hi + 1) : 0;
+
     // Dense value slots in order of first appearance.
-    std::unordered_map<int32_t, uint32_t> slot_of;
+    std::unordered_map<int32_t, uint32_t> slot_map;
+    std::vector<int32_t> slot_flat(n_ids, -1);
     std::vector<int32_t> slot_ids;
     auto note = [&](int32_t id) {
-        if (slot_of.emplace(id, static_cast<uint32_t>(slot_ids.size())).second)
+        if (dense) {
+            int32_t& sl = slot_flat[static_cast<size_t>(id)];
+            if (sl < 0) {
+                sl = static_cast<int32_t>(slot_ids.size());
+                slot_ids.push_back(id);
+            }
+        } else if (slot_map.emplace(id, static_cast<uint32_t>(slot_ids.size())).second) {
             slot_ids.push_back(id);
+        }
+    };
+    auto slot_at = [&](int32_t id) -> uint32_t {
+        if (!dense)
+            return slot_map.at(id);
+        if (id < 0 || static_cast<size_t>(id) >= n_ids || slot_flat[static_cast<size_t>(id)] < 0)
+            throw std::out_of_range("value slot");
+        return static_cast<uint32_t>(slot_flat[static_cast<size_t>(id)]);
     };
     k.for_each_instruction([&](const BasicBlock&, const Instruction& in) {
         if (in.result && *in.result >= 0)
@@ -270,7 +302,7 @@ void BatchImage::add(const Kernel& k) {
             return static_cast<uint16_t>(poison_missing);
         const Operand& o = in.operands[i];
         if (o.kind == Operand::Kind::Value)
-            return static_cast<uint16_t>(slot_of.at(o.value));
+            return static_cast<uint16_t>(slot_at(o.value));
         if (o.kind == Operand::Kind::Param)
             return static_cast<uint16_t>(o.param >= 0 && static_cast<uint32_t>(o.param) < P
                                              ? V + static_cast<uint32_t>(o.param)
@@ -280,7 +312,11 @@ void BatchImage::add(const Kernel& k) {
 
     // Pointer provenance for privatising writable global buffers: pointers
     // only originate from parameters and flow through getindex and phi.
-    std::unordered_map<int32_t, uint64_t> prov;
+    std::unordered_map<int32_t, uint64_t> prov_map;
+    std::vector<uint64_t> prov_flat(n_ids, 0);
+    auto prov_ref = [&](int32_t id) -> uint64_t& {
+        return dense ? prov_flat[static_cast<size_t>(id)] : prov_map[id];
+    };
     auto prov_of = [&](const Operand& o) -> uint64_t {
         if (o.kind == Operand::Kind::Param)
             return (o.param >= 0 && static_cast<uint32_t>(o.param) < P &&
@@ -288,8 +324,10 @@ void BatchImage::add(const Kernel& k) {
                        ? (1ull << o.param)
                        : 0;
         if (o.kind == Operand::Kind::Value) {
-            const auto it = prov.find(o.value);
-            return it == prov.end() ? 0 : it->second;
+            if (dense)
+                return prov_flat[static_cast<size_t>(o.value)];
+            const auto it = prov_map.find(o.value);
+            return it == prov_map.end() ? 0 : it->second;
         }
         return 0;
     };
@@ -306,7 +344,7 @@ void BatchImage::add(const Kernel& k) {
                 for (const Operand& o : in.operands)
                     m |= prov_of(o);
             }
-            uint64_t& cur = prov[*in.result];
+            uint64_t& cur = prov_ref(*in.result);
             if ((cur | m) != cur) {
                 cur |= m;
                 grew = true;
@@ -361,7 +399,7 @@ void BatchImage::add(const Kernel& k) {
                     r = ref(phi, a);
                     break;
                 }
-            out[j] = r | (static_cast<uint32_t>(slot_of.at(*phi.result)) << 16);
+            out[j] = r | (static_cast<uint32_t>(slot_at(*phi.result)) << 16);
         }
         return {out[0], out[1]};
     };
@@ -383,7 +421,7 @@ void BatchImage::add(const Kernel& k) {
             gevo_inst g{};
             g.op = static_cast<uint8_t>(in.op);
             g.cls = cost_class(k, in);
-            g.res = (in.result && *in.result >= 0) ? static_cast<uint16_t>(slot_of.at(*in.result))
+            g.res = (in.result && *in.result >= 0) ? static_cast<uint16_t>(slot_at(*in.result))
                                                    : static_cast<uint16_t>(GEVO_NO_RESULT);
             g.t0 = g.t1 = -1;
             switch (in.op) {
