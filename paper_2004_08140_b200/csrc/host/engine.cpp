@@ -713,7 +713,7 @@ void Engine::step_generation() {
         jobs.resize(slots.size());
         std::vector<Individual> parents(slots.size());
         for (size_t i = 0; i < slots.size(); ++i)
-            parents[i] = offspring[slots[i]];
+            parents[i] = std::move(offspring[slots[i]]); // refilled from the job below
         for (size_t i = 0; i < slots.size(); ++i) {
             jobs[i].parent = &parents[i];
             jobs[i].rng = &rngs[i];
