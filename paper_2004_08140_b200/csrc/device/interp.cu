@@ -1648,6 +1648,10 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
             ok = false;
         } else if (op == GEVO_OP_BR) {
             th.ip = static_cast<int32_t>(pc - b.start);
+#ifndef GEVO_BR_EDGE_LATE
+            // the edge record is in flight while the condition is read
+            const uint4 er = __ldg(reinterpret_cast<const uint4*>(L.edges + pc));
+#endif
             int32_t target = f_t0(r);
             bool second = false;
             if (f_aux(r) == 2) {
@@ -1684,7 +1688,9 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
                     return kStopTrap;
                 }
             }
+#ifdef GEVO_BR_EDGE_LATE
             const uint4 er = __ldg(reinterpret_cast<const uint4*>(L.edges + pc));
+#endif
             if (!enter_block(A, L, th, target, b, S,
                              second ? make_uint2(er.z, er.w) : make_uint2(er.x, er.y)))
                 return kStopTrap;
