@@ -220,16 +220,25 @@ int gevo_batch_create(gevo_suite* s, gevo_batch** out) {
     });
 }
 
+// The resident copy of a batch is dropped before its host image changes; an
+// evaluation still in flight (gevo_eval_resident_async without _wait) reads
+// that image, so changing the batch then is a usage error.
+static void drop_resident(gevo_batch* b) {
+    if (b->resident && b200::resident_pending(*b->resident))
+        throw std::logic_error("batch has an evaluation in flight: call gevo_eval_resident_wait first");
+    b->resident.reset();
+}
+
 int gevo_batch_add_ir(gevo_batch* b, const char* kernel_ir) {
     return guard([&] {
-        b->resident.reset(); // first: it holds a host registration of the blob
+        drop_resident(b); // first: it holds a host registration of the blob
         b->image->add(parse_kernel(kernel_ir));
     });
 }
 
 int gevo_batch_add_patch(gevo_batch* b, const char* patch_json) {
     return guard([&] {
-        b->resident.reset(); // first: it holds a host registration of the blob
+        drop_resident(b); // first: it holds a host registration of the blob
         b->image->add(apply_patch(b->suite->kernel, patch_from_json(patch_json)).kernel);
     });
 }
@@ -297,7 +306,10 @@ int gevo_eval_resident_wait(gevo_batch* b, gevo_variant_record* out_variants, ge
 }
 
 int gevo_batch_make_resident(gevo_batch* b) {
-    return guard([&] { b->resident = b200::make_resident(*b->suite->suite, *b->image); });
+    return guard([&] {
+        drop_resident(b);
+        b->resident = b200::make_resident(*b->suite->suite, *b->image);
+    });
 }
 
 int gevo_eval_resident(gevo_batch* b, const gevo_exec_config* cfg, double tolerance,

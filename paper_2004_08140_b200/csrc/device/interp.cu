@@ -61,6 +61,18 @@ constexpr int64_t kSpinMinJump = 4;
 constexpr uint32_t kTsFresh = 0, kTsResume = 3u << 16; // never run / resume after barrier
 constexpr uint32_t kTsRet = 1u << 16, kTsSync = 2u << 16;
 
+// Instance memory cell meta word (high half of a cell): value tag in bits
+// 0..5 (cells hold only undef / i32 / f32), writer thread id + 1 in bits
+// 6..15 (simulated threads <= kTpMaxBlock = 512 < 1023), phase epoch in bits
+// 16..31 (an instance restarts in id order before the epoch wraps).
+constexpr uint32_t kCellTag = 0x3Fu, kCellWriterShift = 6, kCellWriterMask = 0x3FFu;
+__device__ __forceinline__ uint32_t cell_meta(uint32_t tag, uint32_t writer, uint32_t epoch) {
+    return tag | (writer << kCellWriterShift) | (epoch << 16);
+}
+__device__ __forceinline__ uint32_t cell_writer(uint32_t meta) {
+    return (meta >> kCellWriterShift) & kCellWriterMask;
+}
+
 // Field accessors of the 16-byte record (bytecode.h).
 __device__ __forceinline__ uint32_t f_op(const uint4& r) { return r.x & 0xFF; }
 __device__ __forceinline__ uint32_t f_aux(const uint4& r) { return (r.x >> 8) & 0xFF; }
@@ -565,7 +577,7 @@ __device__ __forceinline__ uint2 mem_word(const InterpArgs& A, const Lane<kM>& L
     const uint32_t eff = key & 0xFFFFFF, space = key >> 24;
     if (Lane<kM>::kTP) {
         const uint2 c = L.cell_get(space == 0x80 ? eff : A.cell_off[space - 1] + eff);
-        return make_uint2(c.x, c.y & 0xFF);
+        return make_uint2(c.x, c.y & kCellTag);
     }
     if (space == 0x80) {
         const size_t at = static_cast<size_t>(eff) * A.n_inst + L.il;
@@ -1173,7 +1185,7 @@ __device__ __forceinline__ bool mem_fast(const InterpArgs& A, Lane<kM>& L, const
         w = static_cast<uint32_t>(eff);
         if (!store) {
             const uint2 x = L.cell_get(w);
-            const uint32_t wt = x.y & 0xFF;
+            const uint32_t wt = x.y & kCellTag;
             if (wt != f_aux(r)) // uninitialised (tag 0) or another type
                 return false;
             if (!L.seq)
@@ -1202,7 +1214,7 @@ __device__ __forceinline__ bool mem_fast(const InterpArgs& A, Lane<kM>& L, const
             if (!L.seq)
                 tp_note(L, w, false);
             tp_read_check(L, x.y);
-            L.W(res, x.x, x.y & 0xFF);
+            L.W(res, x.x, x.y & kCellTag);
             return true;
         }
         if (elem != val.y || !priv)
@@ -1217,14 +1229,14 @@ __device__ __forceinline__ bool mem_fast(const InterpArgs& A, Lane<kM>& L, const
         return true;
     }
     const uint32_t me = static_cast<uint32_t>(L.tid) + 1;
-    const uint32_t meta = val.y | (me << 8) | (L.epoch << 16);
+    const uint32_t meta = cell_meta(val.y, me, L.epoch);
     const unsigned long long want = (static_cast<unsigned long long>(meta) << 32) | val.x;
     const uint2 c0 = L.cell_get(w);
     tp_note(L, w, true);
     unsigned long long cur = (static_cast<unsigned long long>(c0.y) << 32) | c0.x;
     for (;;) {
         const uint32_t m = static_cast<uint32_t>(cur >> 32);
-        if ((m >> 16) == L.epoch && ((m >> 8) & 0xFF) > me)
+        if ((m >> 16) == L.epoch && cell_writer(m) > me)
             break;
         const unsigned long long prev = L.cell_cas(w, cur, want);
         if (prev == cur)
@@ -1246,7 +1258,7 @@ template <int kM>
 __device__ __forceinline__ void tp_read_check(const Lane<kM>& L, uint32_t meta) {
     if (Lane<kM>::kGC || L.seq)
         return;
-    if ((meta >> 16) == (L.epoch & 0xFFFFu) && ((meta >> 8) & 0xFFu) != static_cast<uint32_t>(L.tid) + 1) {
+    if ((meta >> 16) == (L.epoch & 0xFFFFu) && cell_writer(meta) != static_cast<uint32_t>(L.tid) + 1) {
         sts1(L.fsh, 1u);
         asm volatile("red.shared.min.s32 [%0], %1;" ::"r"(L.tsh_star), "r"(L.tid) : "memory");
     }
@@ -1308,13 +1320,13 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
                 tp_note(L, w, false);
             tp_read_check(L, x.y);
             if (p.y == GEVO_TAG_PTR_SHARED) {
-                const uint32_t wt = x.y & 0xFF;
+                const uint32_t wt = x.y & kCellTag;
                 if (wt == GEVO_TAG_UNDEF)
                     return L.trap(GEVO_TRAP_SHARED_UNINIT);
                 if (wt != f_aux(r))
                     return L.trap(GEVO_TRAP_SHARED_TYPE);
             }
-            return L.set(f_res(r), x.x, x.y & 0xFF);
+            return L.set(f_res(r), x.x, x.y & kCellTag);
         }
         if (L.seq) {
             L.cell_put(w, val.x, val.y);
@@ -1324,14 +1336,14 @@ __device__ __forceinline__ bool mem_op(const InterpArgs& A, Lane<kM>& L, const u
         // wins, and a thread's own stores land in program order (the
         // reference runs threads one after another, src/vm.cpp:121-142).
         const uint32_t me = static_cast<uint32_t>(L.tid) + 1;
-        const uint32_t meta = val.y | (me << 8) | (L.epoch << 16);
+        const uint32_t meta = cell_meta(val.y, me, L.epoch);
         const unsigned long long want = (static_cast<unsigned long long>(meta) << 32) | val.x;
         const uint2 c0 = L.cell_get(w);
         tp_note(L, w, true);
         unsigned long long cur = (static_cast<unsigned long long>(c0.y) << 32) | c0.x;
         for (;;) {
             const uint32_t m = static_cast<uint32_t>(cur >> 32);
-            if ((m >> 16) == L.epoch && ((m >> 8) & 0xFF) > me)
+            if ((m >> 16) == L.epoch && cell_writer(m) > me)
                 break;
             const unsigned long long prev = L.cell_cas(w, cur, want);
             if (prev == cur)

@@ -629,6 +629,10 @@ struct ResidentBatch {
     const void* reg = nullptr;
     size_t reg_size = 0;
     ~ResidentBatch() {
+        // an evaluation still in flight reads the blob and writes the pinned
+        // record buffer: let it finish before either is released
+        if (pending && done)
+            cudaEventSynchronize(done);
         if (reg)
             cudaHostUnregister(const_cast<void*>(reg));
         if (stream)
@@ -710,6 +714,8 @@ void evaluate_resident_async(ResidentBatch& rb, const ExecImage& exec, const Eva
 }
 
 uint64_t resident_h2d(const ResidentBatch& rb) { return rb.h2d; }
+
+bool resident_pending(const ResidentBatch& rb) { return rb.pending; }
 
 float wait_resident(ResidentBatch& rb, std::vector<gevo_variant_record>* out, int* launches) {
     if (!rb.pending)

@@ -91,6 +91,7 @@ void evaluate_resident_async(ResidentBatch& rb, const ExecImage& exec, const Eva
                              const std::vector<uint8_t>* upload = nullptr);
 float wait_resident(ResidentBatch& rb, std::vector<gevo_variant_record>* out, int* launches);
 uint64_t resident_h2d(const ResidentBatch& rb);
+bool resident_pending(const ResidentBatch& rb);
 float evaluate_resident(ResidentBatch& rb, const ExecImage& exec, const EvalOptions& opt,
                         float* interp_ms, std::vector<gevo_variant_record>* out,
                         int* launches = nullptr);
