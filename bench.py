@@ -1,35 +1,44 @@
 """Benchmark of the GEVO fitness-evaluation hot path on B200.
 
-Workload (BASELINE.json configs[1], "config 2"): the Rodinia-style corpus
-kernels hot-branch (hotspot), nw-sync (nw) and bfs-load (bfs); per kernel one
-candidate batch of 1024 validated mutants -- the ~1016 `sanity_check` calls of
-one pop-256 generation -- drawn as seeded random walks by the
-product host, evaluated on the 16 synthetic train inputs of
-generate_tests(b, 16, train_seed(1)) with the default 10^6 instruction budget
-and tolerance 0 (mode default). One step = evaluate_fitness of all three
-batches (3 x 1024 variants x 16 tests) on the device.
+Headline workload (BASELINE.json configs[3], "config 4", the largest
+single-GPU configuration): a candidate batch of 4096 validated mutants
+(seeded random walks of up to 3 edits, the search's candidate stream;
+bench_data/cand_conv-bn_s1.txt.gz) of the authored conv3x3 + bias + batch-norm
+IR kernel (paper_2004_08140_b200/data/kernels/conv-bn: CIFAR-shaped
+in[3x32x32] f32, w[64x3x3x3] -> out[64x32x32], 256 simulated threads) on the 3
+seeded train inputs of generate_tests_for(kernel, spec, 3, train_seed(1)),
+budget 10^6 instructions per simulated thread, tolerance 0.01, early exit
+(the reference's evaluate_fitness stops at a variant's first failing test).
+One step = evaluate_fitness of the whole batch on the device.
 
-metric: variant x input evaluations/s = reference-equivalent executions
-(tests the reference's evaluate_fitness runs: all of an accepted variant's,
+metric: variant x input evaluations/s = reference-equivalent executions (the
+tests the reference's evaluate_fitness runs: all of an accepted variant's,
 else up to and including the first failing one) per second; IR instrs/s is
-reported beside it. `value` times device-resident batches (CUDA events on the
-launch stream, L2 flushed between steps); `e2e` times the C-ABI call with
-host bytecode (H2D of the batch, D2H of the records inside the timed region).
-The three batches are independent and are evaluated concurrently, each on its
-own stream (gevo_eval_resident_async / _wait), so their launch tails overlap.
+reported beside it (reference-equivalent, and device-executed).
+`value`: device-resident batch, CUDA events on the launching stream (the
+caller's stream: the library launches on it, gevo_set_stream), L2 flushed by a
+512 MiB write on that stream before every timed step. `e2e`: the same through
+the C ABI with host bytecode -- H2D of the batch image and D2H of the records
+inside the timed region. Validation is outside both arms' timed regions.
 
---impl reference times the reference's own CPU path (oracle/_ref/ref_bench:
-validate + evaluate_fitness from /root/reference/proj/src compiled in place)
-on the same candidate files with every host core.
+Config 2 (configs[1]: hot-branch / nw-sync / bfs-load, 1024 mutants each x 16
+tests, tol 0) is measured in the same run and reported in `secondary`.
 
-Multi-GPU (torchrun, one process per GPU, NCCL): weak scaling -- each rank
-evaluates its own candidate batches (seed 1 + rank); the per-variant fitness
-records are exchanged with an NCCL all-gather and the gathered population is
-ranked by the GPU non-dominated sort (the north star's only exchange step).
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/ref_bench: /root/reference/proj/src compiled in place,
+evaluate_fitness) on the same committed candidates with every host core, each
+step a bounded sample; that arm never loads the product library.
+
+Multi-GPU (torchrun, one process per GPU, NCCL): weak scaling -- rank r
+evaluates its own 4096-candidate batch (seed 1 + r); the per-variant fitness
+rows are exchanged with an NCCL all-gather, then rank_population +
+select_best of the gathered pool run on the GPU (the north star's only
+exchange step).
 """
 from __future__ import annotations
 
 import argparse
+import gzip
 import json
 import os
 import shutil
@@ -43,28 +52,35 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-KERNELS = ("hot-branch", "nw-sync", "bfs-load")
-N_VARIANTS = 1024
-N_TESTS = 16
-MASTER_SEED = 1
-MAX_DEPTH = 4
 METRIC = "variant x input evaluations/s"
 UNIT = "evals/s"
 REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
 ISSUE_PROFILE = os.path.join(ROOT, "profiles", "issue_per_launch.json")
+BENCH_DATA = os.path.join(ROOT, "bench_data")
+KERNEL_DIR = os.path.join(ROOT, "paper_2004_08140_b200", "data", "kernels")
+MASTER_SEED = 1
+
+C4 = {"name": "config4", "kernel": "conv-bn", "variants": 4096, "tests": 3, "tol": 0.01,
+      "budget": 1_000_000, "depth": 3}
+C2 = {"name": "config2", "kernels": ("hot-branch", "nw-sync", "bfs-load"), "variants": 1024,
+      "tests": 16, "tol": 0.0, "budget": 1_000_000, "depth": 4}
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--variants", type=int, default=N_VARIANTS)
-    ap.add_argument("--tests", type=int, default=N_TESTS)
     ap.add_argument("--cpu-seconds", type=float, default=20.0,
                     help="bound of the cpu_baseline sample")
+    ap.add_argument("--ref-step-seconds", type=float, default=8.0,
+                    help="--impl reference: bound of each step's sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--profile-step", choices=["config4", "config2"],
+                    help="one untimed step of that workload between cudaProfilerStart/Stop "
+                         "(ncu --profile-from-start off), then exit")
     return ap.parse_args()
 
 
@@ -73,48 +89,65 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", "1")))
 
 
-def workload_config(args, world, backend="nccl"):
+def splitmix64(x):
+    m = (1 << 64) - 1
+    x = (x + 0x9E3779B97F4A7C15) & m
+    z = x
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
+def train_seed(master):
+    """src/cli_app.cpp:193-201 (the product exports the same as gevo_train_seed)."""
+    return splitmix64(master ^ 0x7261696E5F736574)
+
+
+def c4_config(world, backend="nccl"):
     return {
-        "workload": "config2: GEVO candidate batches, Rodinia-style IR kernels "
-                    "hot-branch/nw-sync/bfs-load, %d validated mutants per kernel x %d "
-                    "synthetic test inputs, budget 1e6, tol 0, seed %d" %
-                    (args.variants, args.tests, MASTER_SEED),
-        "kernels": list(KERNELS),
-        "variants_per_kernel_per_gpu": args.variants,
-        "tests": args.tests,
-        "budget": 1_000_000,
-        "tolerance": 0.0,
-        "parallelism": "population-sharded dp%d (fitness records all-gathered over %s)" %
+        "workload": "config4: GEVO candidate batch of %d validated mutants of the conv3x3+bias+"
+                    "batch-norm IR kernel (CIFAR-shaped in[3x32x32] -> out[64x32x32] f32, 256 "
+                    "simulated threads) x %d synthetic inputs, budget 1e6, tol %g, early exit, "
+                    "seed %d" % (C4["variants"], C4["tests"], C4["tol"], MASTER_SEED),
+        "kernel": C4["kernel"],
+        "variants_per_gpu": C4["variants"],
+        "tests": C4["tests"],
+        "budget": C4["budget"],
+        "tolerance": C4["tol"],
+        "parallelism": "population-sharded dp%d (fitness rows all-gathered over %s, GPU "
+                       "rank_population + select_best of the gathered pool)" %
                        (world, "NCCL" if backend == "nccl" else backend),
-        "l2": "flushed between timed steps (512 MiB write)",
+        "l2": "flushed before every timed step (512 MiB write on the launching stream)",
     }
 
 
-def write_candidates(gevo, seed, n, outdir):
-    files = {}
-    for k in KERNELS:
-        lines = gevo.sample_candidates(k, n, seed, MAX_DEPTH)
-        path = os.path.join(outdir, "cand_%s_%d.txt" % (k, seed))
-        with open(path, "w") as f:
-            f.write("\n".join(lines) + "\n")
-        files[k] = (path, lines)
-    return files
+def committed_candidates(kind, seed=MASTER_SEED):
+    path = os.path.join(BENCH_DATA, "cand_%s_s%d.txt.gz" % (kind, seed))
+    if not os.path.exists(path):
+        return None
+    with gzip.open(path, "rt") as f:
+        return [ln for ln in f.read().splitlines() if ln.strip()]
 
 
-def run_ref_bench(files, n_tests, test_seed, threads, max_seconds):
-    """Reference CPU path over every kernel's candidates; returns totals."""
+def run_ref_bench(target, cand_lines, n_tests, seed, threads, seconds, budget, tol, start=0,
+                  count=True):
+    """The reference's evaluate_fitness over candidates (oracle/_ref/ref_bench)."""
     if not os.path.exists(REF_BENCH):
-        raise RuntimeError("oracle/_ref/ref_bench missing: run __graft_entry__.build() "
-                           "in the container that has /root/reference")
-    tot = {"executions": 0, "ir": 0, "seconds": 0.0, "variants": 0}
-    per = max_seconds / len(files)
-    for k, (path, _) in files.items():
-        out = subprocess.run([REF_BENCH, k, path, str(n_tests), str(test_seed), str(threads),
-                              str(per)], check=True, capture_output=True, text=True).stdout
-        r = json.loads(out.strip().splitlines()[-1])
-        for key in tot:
-            tot[key] += r[key]
-    return tot
+        raise RuntimeError("oracle/_ref/ref_bench missing: run __graft_entry__.build() in the "
+                           "container that has /root/reference (it travels with the repo)")
+    with tempfile.NamedTemporaryFile("w", suffix=".txt", delete=False) as f:
+        f.write("\n".join(cand_lines) + "\n")
+        path = f.name
+    try:
+        env = dict(os.environ)
+        if not count:
+            env["REF_BENCH_NOCOUNT"] = "1"
+        out = subprocess.run([REF_BENCH, target, path, str(n_tests), str(seed), str(threads),
+                              str(seconds), str(budget), str(tol), str(start)],
+                             check=True, capture_output=True, text=True, env=env).stdout
+    finally:
+        os.unlink(path)
+    return json.loads(out.strip().splitlines()[-1])
 
 
 class ClockSampler:
@@ -169,39 +202,100 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ---------------------------------------------------------------------------
+# reference arm: the reference's CPU path, no product code loaded
+
+
 def reference_arm(args):
     rank, _, world = dist_env()
     if rank != 0:
         return
-    import paper_2004_08140_b200 as gevo
+    cands = committed_candidates(C4["kernel"])
+    if cands is None:
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "bench_data/cand_conv-bn_s1.txt.gz missing"}))
+        return
     threads = os.cpu_count() or 1
-    with tempfile.TemporaryDirectory() as tmp:
-        files = write_candidates(gevo, MASTER_SEED, args.variants, tmp)
-        seed = gevo.train_seed(MASTER_SEED)
-        budget = max(args.cpu_seconds, 5.0) * 3
-        for _ in range(args.warmup):
-            run_ref_bench(files, args.tests, seed, threads, budget)
-        tot = {"executions": 0, "ir": 0, "seconds": 0.0, "variants": 0}
-        for _ in range(args.steps):
-            r = run_ref_bench(files, args.tests, seed, threads, budget)
+    target = "file:" + os.path.join(KERNEL_DIR, C4["kernel"])
+    seed = train_seed(MASTER_SEED)
+    tot = {"executions": 0, "ir": 0, "seconds": 0.0, "variants": 0}
+    ir_s = None
+    # each step: a bounded sample of the batch, starting at a different variant
+    stride = 97
+    for i in range(args.warmup + args.steps):
+        r = run_ref_bench(target, cands, C4["tests"], seed, threads, args.ref_step_seconds,
+                          C4["budget"], C4["tol"], start=(i * stride) % len(cands),
+                          count=i == args.warmup)
+        if i == args.warmup:
+            ir_s = r["ir"] / r["seconds"]
+        if i >= args.warmup:
             for k in tot:
                 tot[k] += r[k]
     value = tot["executions"] / tot["seconds"]
-    sample = ("%d of %d candidates per step (3 kernels x %d) x %d tests, evaluate_fitness "
-              "with early exit, %d threads" % (tot["variants"] // max(args.steps, 1),
-                                               3 * args.variants, args.variants, args.tests,
-                                               threads))
+    sample = ("per step %.0f variants of the %d-candidate batch (from a rotating start) x %d "
+              "inputs, reference evaluate_fitness with early exit (validation untimed), "
+              "%d threads, %.0f s bound" % (tot["variants"] / max(args.steps, 1), len(cands),
+                                            C4["tests"], threads, args.ref_step_seconds))
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * tot["seconds"] / max(args.steps, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "i32/f32",
-        "data": "synthetic", "config": workload_config(args, 1),
-        "ir_per_s": tot["ir"] / tot["seconds"],
+        "data": "synthetic (seeded generate_tests_for inputs, committed seeded mutant walks)",
+        "config": c4_config(1),
+        "ir_per_s": ir_s,  # IR counted (untimed re-run at unit cost) on the first timed step
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+
+def issue_profile(workload):
+    if not os.path.exists(ISSUE_PROFILE):
+        return None
+    prof = json.load(open(ISSUE_PROFILE))
+    return prof.get("workloads", {}).get(workload)
+
+
+def roofline_of(workload, step_ms, f_mhz, ir_ref_step, ir_dev_step):
+    """Issue-slot roofline: the interpreter is integer dispatch
+    with per-test working sets on chip. achieved = SASS warp instructions the
+    step's interpreter launches issue (ncu smsp__inst_executed.sum summed over
+    the launches of one step, profiles/issue_per_launch.json) / the step's
+    CUDA-event time; peak = 148 SM x 4 schedulers x 1 warp-instruction/cycle at
+    the median SM clock under load."""
+    peak = 148 * 4 * f_mhz * 1e6 / 1e9
+    prof = issue_profile(workload)
+    out = {"bound": "issue", "achieved": None, "peak": peak, "unit": "Gwarp-inst/s",
+           "frac": None, "traffic": None, "traffic_unit": "DRAM bytes per step (ncu)",
+           "note": "peak = 148 SM x 4 schedulers x 1 warp-inst/cycle x median SM clock"}
+    if not prof or not step_ms:
+        return out
+    achieved = prof["warp_inst"] / (step_ms / 1e3) / 1e9
+    out.update({"achieved": achieved, "frac": achieved / peak, "traffic": prof.get("dram_bytes"),
+                "launches_profiled": prof.get("launches"),
+                "lanes_per_warp_inst": (prof["thread_inst"] / prof["warp_inst"])
+                if prof.get("thread_inst") else None,
+                "ncu_ms_per_step": prof.get("ncu_ms")})
+    # share of the issued work the reference would also execute (speculative
+    # tests after a variant's first failure are discarded)
+    if ir_dev_step:
+        out["useful_ir_fraction"] = ir_ref_step / ir_dev_step
+        out["useful_frac"] = out["frac"] * out["useful_ir_fraction"]
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        hbm_peak, src = peaks["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        hbm_peak, src = 7700.0, "B200_PROFILING.md fallback"
+    if prof.get("dram_bytes") is not None:
+        gbs = prof["dram_bytes"] / (step_ms / 1e3) / 1e9
+        out["hbm_view"] = {"achieved_gbs": gbs, "peak_gbs": hbm_peak, "frac": gbs / hbm_peak,
+                           "peak_source": src}
+    return out
 
 
 def b200_arm(args):
@@ -211,13 +305,10 @@ def b200_arm(args):
     from paper_2004_08140_b200 import dist as gdist
 
     rank, local, world = dist_env()
-    # one process per GPU; more ranks than GPUs (a functional check of the
-    # N > 1 path on a smaller box) share devices round-robin
     shared = world > torch.cuda.device_count()
     local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     os.environ["GEVO_DEVICE"] = str(local)
-    # NCCL needs a distinct GPU per rank: ranks sharing a device exchange over gloo
     backend = os.environ.get("BENCH_DIST_BACKEND", "gloo" if shared else "nccl")
     coll_dev = "cuda" if backend == "nccl" else "cpu"
     if world > 1:
@@ -226,67 +317,62 @@ def b200_arm(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    stream = torch.cuda.current_stream()
+    # every library launch goes to this stream, so CUDA events recorded on it
+    # bracket the work (and the L2 flush on it precedes the work)
+    stream = torch.cuda.Stream()
     gevo.set_stream(stream.cuda_stream)
-
-    tmp = tempfile.mkdtemp(prefix="gevo_bench_")
-    files = write_candidates(gevo, MASTER_SEED + rank, args.variants, tmp)
     seed = gevo.train_seed(MASTER_SEED)
-    suites, batches, cfgs = {}, {}, {}
-    for k in KERNELS:
-        suites[k] = gevo.Suite.from_benchmark(k, args.tests, seed)
-        cfgs[k] = suites[k].exec_config()
-        b = suites[k].batch()
-        for line in files[k][1]:
-            b.add_patch(line)
-        b.make_resident()
-        batches[k] = b
+    assert seed == train_seed(MASTER_SEED)
 
+    # ---- config 4 batch
+    ir, gen = gevo.authored_kernel(C4["kernel"])
+    cands = committed_candidates(C4["kernel"], MASTER_SEED + rank)
+    if cands is None:
+        cands = gevo.sample_candidates_ir(ir, C4["variants"], MASTER_SEED + rank, C4["depth"])
+    suite = gevo.Suite.from_spec(ir, gen, C4["tests"], seed)
+    cfg = suite.exec_config().with_(budget=C4["budget"])
+    batch = suite.batch()
+    for line in cands:
+        batch.add_patch(line)
+    batch.make_resident()
+
+    # ---- config 2 batches (secondary)
+    c2 = {}
+    if not args.no_secondary and not args.profile_step == "config4":
+        for k in C2["kernels"]:
+            lines = committed_candidates(k, MASTER_SEED + rank) or \
+                gevo.sample_candidates(k, C2["variants"], MASTER_SEED + rank, C2["depth"])
+            s2 = gevo.Suite.from_benchmark(k, C2["tests"], seed)
+            b2 = s2.batch()
+            for line in lines:
+                b2.add_patch(line)
+            b2.make_resident()
+            c2[k] = (s2, b2, s2.exec_config())
+
+    if args.profile_step:
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        if args.profile_step == "config4":
+            batch.eval_resident(cfg, tolerance=C4["tol"], early_exit=True, records=True)
+        else:
+            for k in C2["kernels"]:
+                c2[k][1].eval_resident_async(c2[k][2], tolerance=C2["tol"], early_exit=True)
+            for k in C2["kernels"]:
+                c2[k][1].wait(records=True)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        print(json.dumps({"profile_step": args.profile_step}))
+        return
+
+    # untimed pass with per-test records: reference-equivalent and
+    # device-executed work of one step
     gevo.spin_counters(reset=True)
-    # One untimed pass with per-test records: device-executed IR (speculative
-    # work included) for the issue-rate roofline.
-    dev_ir = 0
-    ref_execs_step = ref_ir_step = 0
-    for k in KERNELS:
-        v, t, _ = batches[k].eval(cfgs[k], tolerance=0.0, early_exit=True, tests=True)
-        dev_ir += int(t["ir"].sum())
-        ref_execs_step += int(v["execs_ref"].sum())
-        ref_ir_step += int(v["ir_ref"].sum())
-
+    v, t, _ = batch.eval(cfg, tolerance=C4["tol"], early_exit=True, tests=True)
+    execs_step = int(v["execs_ref"].sum())
+    ir_ref_step = int(v["ir_ref"].sum())
+    ir_dev_step = int(t["ir"][t["status"] != 3].sum())
     spins = gevo.spin_counters(reset=True)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-
-    gathered_front = None
-
-    def exchange(vrec_list):
-        # NCCL all-gather of per-variant fitness (cost_mean, error_max, accepted)
-        # then the GPU non-dominated sort of the gathered population.
-        nonlocal gathered_front
-        rows = gdist.fitness_rows(np.concatenate(vrec_list))
-        g = gdist.allgather_fitness(rows, device=coll_dev) if world > 1 else rows
-        cost, err, _ = gdist.accepted_fitness(g)
-        front, _, _ = gevo.rank(cost, err)
-        gathered_front = front
-
-    timed_launches = [0]
-    kernel_ms = {k: [] for k in KERNELS}
-
-    # launch order of the concurrent batches (records are still gathered in
-    # KERNELS order)
-    order = os.environ.get("BENCH_LAUNCH_ORDER", ",".join(KERNELS)).split(",")
-
-    def step_resident():
-        # the three batches are independent: each runs on its own stream and
-        # their launches (and launch tails) overlap on the GPU
-        for k in order:
-            batches[k].eval_resident_async(cfgs[k], tolerance=0.0, early_exit=True)
-        recs = []
-        for k in KERNELS:
-            v, st = batches[k].wait(records=True)
-            timed_launches[0] += st.launches
-            kernel_ms[k].append(st.device_ms)
-            recs.append(v)
-        return recs
 
     def barrier():
         if world > 1:
@@ -294,158 +380,194 @@ def b200_arm(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        exchange(step_resident())
-    barrier()
+    def exchange(vrec):
+        # NCCL all-gather of per-variant fitness (cost_mean, error_max,
+        # accepted), then rank_population + select_best of the gathered pool
+        rows = gdist.fitness_rows(vrec)
+        g = gdist.allgather_fitness(rows, device=coll_dev) if world > 1 else rows
+        cost, err, _ = gdist.accepted_fitness(g)
+        keep = len(cost) * 4 // 5
+        return gevo.select_best(cost, err, keep)
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    timed_launches[0] = 0
-    for k in KERNELS:
-        kernel_ms[k].clear()
-    with ClockSampler(local) as clocks:
-        for i in range(args.steps):
-            flush.fill_(i & 0xFF)
-            ev[i][0].record(stream)
-            recs = step_resident()
-            ev[i][1].record(stream)
-            exchange(recs)
+    def timed(step_fn, k, w):
+        for _ in range(w):
+            step_fn(None)
         barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(k)]
+        for i in range(k):
+            step_fn(ev[i])
+        barrier()
+        return [a.elapsed_time(b) for a, b in ev]
+
+    lib_ms, launches, rank_ms = [], [0], []
+
+    def step_resident(ev):
+        with torch.cuda.stream(stream):
+            flush.fill_(1)
+            if ev:
+                ev[0].record(stream)
+            vrec, st = batch.eval_resident(cfg, tolerance=C4["tol"], early_exit=True, records=True)
+            if ev:
+                ev[1].record(stream)
+                lib_ms.append(st.device_ms)
+                launches[0] += st.launches
+        _, ms = exchange(vrec)
+        if ev:
+            rank_ms.append(ms)
+
+    with ClockSampler(local) as clocks:
+        step_ms = timed(step_resident, args.steps, args.warmup)
     dev_ms = sum(step_ms)
 
-    # e2e through the C ABI with host bytecode (H2D + kernels + D2H records)
-    def step_e2e():
-        for k in order:
-            batches[k].eval_resident_async(cfgs[k], tolerance=0.0, early_exit=True, upload=True)
-        return [batches[k].wait(records=True)[1] for k in KERNELS]
-
-    for _ in range(args.warmup):
-        step_e2e()
-    barrier()
     h2d = d2h = 0
-    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    launches = 0
-    for i in range(args.steps):
-        flush.fill_(i & 0xFF)
-        ev2[i][0].record(stream)
-        h2d = d2h = 0
-        # C-ABI evaluations with the host bytecode uploaded inside the timed
-        # region and the records read back, the three batches concurrently
-        for st in step_e2e():
-            h2d += st.h2d_bytes
-            d2h += st.d2h_bytes
-            launches += st.launches
-        ev2[i][1].record(stream)
-    barrier()
-    e2e_ms = sum(a.elapsed_time(b) for a, b in ev2)
+    e2e_launches = [0]
+
+    def step_e2e(ev):
+        nonlocal h2d, d2h
+        with torch.cuda.stream(stream):
+            flush.fill_(2)
+            if ev:
+                ev[0].record(stream)
+            batch.eval_resident_async(cfg, tolerance=C4["tol"], early_exit=True, upload=True)
+            _, st = batch.wait(records=True)
+            if ev:
+                ev[1].record(stream)
+                h2d, d2h = st.h2d_bytes, st.d2h_bytes
+                e2e_launches[0] += st.launches
+
+    e2e_ms = sum(timed(step_e2e, args.steps, args.warmup))
+
+    # host pipeline beside it (diagnostic, wall clock, one pass): patches ->
+    # apply_patch + encode -> H2D -> evaluate -> records
+    t0 = time.perf_counter()
+    b_host = suite.batch()
+    for line in cands:
+        b_host.add_patch(line)
+    t1 = time.perf_counter()
+    b_host.eval(cfg, tolerance=C4["tol"], early_exit=True)
+    t2 = time.perf_counter()
+    host_pipeline = {"encode_s": t1 - t0, "eval_s": t2 - t1,
+                     "value": execs_step / (t2 - t0), "unit": UNIT,
+                     "note": "patches applied, encoded, uploaded and evaluated through the C ABI "
+                             "(wall clock, one pass)"}
+    del b_host
+
+    sec = None
+    if c2:
+        sec = secondary_config2(args, gevo, torch, stream, flush, c2, barrier, world)
 
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=coll_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms, e2e_ms = t.tolist()
+        tt = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=coll_dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dev_ms, e2e_ms = tt.tolist()
 
-    total_execs = ref_execs_step * args.steps * world
+    total_execs = execs_step * args.steps * world
     value = total_execs / (dev_ms / 1000.0)
     e2e_value = total_execs / (e2e_ms / 1000.0)
-
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
         return
 
-    # Roofline: the interpreter is issue-slot bound -- integer
-    # dispatch, no dense contraction, per-test working sets that live on chip.
-    # achieved = SASS warp instructions the interpreter launches issue per step
-    # (smsp__inst_executed.sum per launch, ncu, profiles/issue_per_launch.json)
-    # / the step's CUDA-event time measured here (the batches run concurrently); peak = 148 SM x 4
-    # schedulers x 1 warp instruction per cycle at the median SM clock under
-    # load. traffic = DRAM bytes per launch of the dominant (hot-branch) launch.
     ck = clocks.summary()
     f_mhz = ck["sm_mhz"] or 1965.0
-    peak = 148 * 4 * f_mhz * 1e6 / 1e9
-    achieved = traffic = None
-    per_kernel = {}
-    if os.path.exists(ISSUE_PROFILE):
-        prof = json.load(open(ISSUE_PROFILE))["kernels"]
-        inst = sum(prof[k]["warp_inst"] for k in KERNELS if k in prof)
-        # the three batches overlap on the GPU: the step time (CUDA events on
-        # the launch stream) is the time their launches take together
-        live_ms = dev_ms / args.steps
-        if inst and live_ms and all(k in prof for k in KERNELS):
-            achieved = inst / (live_ms / 1e3) / 1e9
-        dom = prof.get(KERNELS[0], {})
-        traffic = dom.get("dram_bytes")
-        for k in KERNELS:
-            if k in prof:
-                per_kernel[k] = {"live_ms": round(statistics.mean(kernel_ms[k]), 4),
-                                 "ncu_ms": prof[k].get("ncu_ms"),
-                                 "warp_inst": prof[k]["warp_inst"],
-                                 "lanes_per_warp_inst": (prof[k]["thread_inst"] /
-                                                         prof[k]["warp_inst"])
-                                 if prof[k].get("thread_inst") else None}
-    # Secondary (HBM) view: DRAM bytes the interpreter launches move (ncu, per
-    # launch) over their live time, against the measured copy bandwidth. The
-    # per-test working sets (<= ~5 KB) stay in L2 / shared memory, so this is
-    # tiny by construction -- the interpreter is not memory-bound.
-    hbm_view = None
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        hbm_peak, hbm_src = peaks["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs"
-    except (OSError, KeyError, ValueError):
-        hbm_peak, hbm_src = 7700.0, "B200_PROFILING.md fallback"
-    if per_kernel and os.path.exists(ISSUE_PROFILE):
-        prof = json.load(open(ISSUE_PROFILE))["kernels"]
-        dram = sum(prof[k].get("dram_bytes") or 0 for k in KERNELS if k in prof)
-        live_ms = dev_ms / args.steps
-        gbs = dram / (live_ms / 1e3) / 1e9 if live_ms else 0.0
-        hbm_view = {"achieved_gbs": gbs, "peak_gbs": hbm_peak, "frac": gbs / hbm_peak,
-                    "peak_source": hbm_src}
-    roofline = {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "traffic_unit": "DRAM bytes per hot-branch launch (ncu)",
-                "per_kernel": per_kernel,
-                "hbm_view": hbm_view,
-                "note": "peak = 148 SM x 4 schedulers x 1 warp-inst/cycle x median SM clock"}
+    roofline = roofline_of("config4", dev_ms / args.steps, f_mhz, ir_ref_step, ir_dev_step)
+    roofline["lib_ms_per_step"] = statistics.mean(lib_ms) if lib_ms else None
 
     cpu = None
     if not args.no_cpu_baseline and world == 1 and os.path.exists(REF_BENCH):
         threads = os.cpu_count() or 1
-        r = run_ref_bench(files, args.tests, seed, threads, args.cpu_seconds)
+        r = run_ref_bench("file:" + os.path.join(KERNEL_DIR, C4["kernel"]), cands, C4["tests"],
+                          seed, threads, args.cpu_seconds, C4["budget"], C4["tol"], count=False)
         cpu = {"value": r["executions"] / r["seconds"], "unit": UNIT, "cores": threads,
                "kind": "reference",
-               "sample": "%d of %d candidates (3 kernels) x %d tests, reference validate + "
-                         "evaluate_fitness, %.1f s bound" % (r["variants"], 3 * args.variants,
-                                                             args.tests, args.cpu_seconds),
-               "ir_per_s": r["ir"] / r["seconds"]}
-    shutil.rmtree(tmp, ignore_errors=True)
+               "sample": "first %d of %d candidates x %d inputs, reference evaluate_fitness "
+                         "(validation untimed), %.0f s bound" %
+                         (r["variants"], len(cands), C4["tests"], args.cpu_seconds)}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "i32/f32 (IEEE, no FMA) + f64 error",
-        "data": "synthetic (seeded generate_tests inputs, seeded mutant walks)",
-        "config": workload_config(args, world, backend),
-        "ir_per_s": ref_ir_step * args.steps * world / (dev_ms / 1000.0),
-        "executions_per_step": ref_execs_step * world,
+        "data": "synthetic (seeded generate_tests_for inputs, committed seeded mutant walks)",
+        "config": c4_config(world, backend),
+        "executions_per_step": execs_step * world,
+        "ir_per_s": ir_ref_step * args.steps * world / (dev_ms / 1000.0),
+        "device_ir_per_s": ir_dev_step * args.steps * world / (dev_ms / 1000.0),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": timed_launches[0],
-        "gpu_launches_e2e": launches,
+        "gpu_launches": launches[0],
+        "gpu_launches_e2e": e2e_launches[0],
         "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": ck,
-        "step_ms": [round(x, 4) for x in step_ms],
+        "step_ms": [round(x, 3) for x in step_ms],
+        "rank_select_ms": round(statistics.mean(rank_ms), 4) if rank_ms else None,
+        "host_pipeline": host_pipeline,
         "spin_accelerator": {"loops_jumped_per_step": spins[0],
                              "instructions_skipped_per_step": spins[1]},
+        "secondary": sec,
     }
     print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def secondary_config2(args, gevo, torch, stream, flush, c2, barrier, world):
+    """Config 2: the three corpus batches evaluated concurrently (each on its
+    own stream, ordered after the caller's stream) -- value and e2e."""
+    ks = C2["kernels"]
+    execs = ir_ref = 0
+    for k in ks:
+        s2, b2, cfg2 = c2[k]
+        v, _, _ = b2.eval(cfg2, tolerance=C2["tol"], early_exit=True)
+        execs += int(v["execs_ref"].sum())
+        ir_ref += int(v["ir_ref"].sum())
+
+    def run(upload, ev):
+        with torch.cuda.stream(stream):
+            flush.fill_(3)
+            if ev:
+                ev[0].record(stream)
+            for k in ks:
+                c2[k][1].eval_resident_async(c2[k][2], tolerance=C2["tol"], early_exit=True,
+                                             upload=upload)
+            sts = [c2[k][1].wait(records=True)[1] for k in ks]
+            if ev:
+                ev[1].record(stream)
+        return sts
+
+    def timed(upload):
+        for _ in range(args.warmup):
+            run(upload, None)
+        barrier()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        live = []
+        for i in range(args.steps):
+            sts = run(upload, ev[i])
+            live.append(max(s.device_ms for s in sts))
+        barrier()
+        return [a.elapsed_time(b) for a, b in ev], live
+
+    steps, live = timed(False)
+    e2e_steps, _ = timed(True)
+    ms = statistics.mean(steps)
+    return {
+        "workload": "config2: hot-branch/nw-sync/bfs-load, %d validated mutants each x %d "
+                    "synthetic inputs, budget 1e6, tol 0, the three batches concurrently" %
+                    (C2["variants"], C2["tests"]),
+        "value": execs * world / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+        "e2e": {"value": execs * world / (statistics.mean(e2e_steps) / 1e3), "unit": UNIT},
+        "ir_per_s": ir_ref * world / (ms / 1e3),
+        "executions_per_step": execs * world,
+        "batch_live_ms_max": round(max(live), 4),
+        "roofline": roofline_of("config2", ms, 1965.0, ir_ref, None),
+    }
 
 
 def main():

@@ -175,6 +175,12 @@ int gevo_nsga_select(const double* cost, const double* error, int32_t n, int dev
                      int32_t keep, int32_t* best_out, uint64_t tournament_seed, int32_t k,
                      int32_t* tournament_out);
 
+/* rank_population + select_best(rank, keep) (nsga.cpp:88-106, 126-148) in one
+ * device pass: only the keep order crosses back. device_ms (nullable) = CUDA-
+ * event time of the ranking kernels. */
+int gevo_select_best(const double* cost, const double* error, int32_t n, int device, int32_t keep,
+                     int32_t* best_out, float* device_ms);
+
 /* ---- host-side API of the search (no device work) ------------------------ */
 int gevo_kernel_canonical(const char* kernel_ir, char** printed);          /* parse + print */
 int gevo_kernel_validate(const char* kernel_ir, char** rules_json);        /* validate() */

@@ -1,13 +1,18 @@
 // CPU baseline driver. TEST/BENCH INFRASTRUCTURE ONLY.
 //
-// Times the reference's own fitness path (Engine::sanity_check semantics:
-// validate + evaluate_fitness, src/engine.cpp:91-95 and src/vm.cpp:558-579)
-// over a workload of variants, on the host cores, with a plain std::thread
-// pool (the reference's parallel_for shape, src/engine.cpp:28-62). Used by
-// bench.py for the `cpu_baseline` field and for `--impl reference`.
+// Times the reference's own fitness evaluation (evaluate_fitness,
+// src/vm.cpp:558-579, the evaluation half of Engine::sanity_check,
+// src/engine.cpp:91-95) over a workload of variants, on the host cores, with a
+// plain std::thread pool (the reference's parallel_for shape,
+// src/engine.cpp:28-62). Validation (is_valid) runs before the timed region,
+// as the device arm's timed region holds evaluation only. Used by bench.py for
+// the `cpu_baseline` field and for `--impl reference`.
 //
 //   ref_bench <bench> <variants.txt> <n_tests> <test_seed> <threads> <max_seconds>
-//             [budget=1000000] [tolerance=0]
+//             [budget=1000000] [tolerance=0] [start=0]
+//
+// start: first variant of the sample (the timed loop walks the variants from
+// there, wrapping around, until max_seconds).
 //
 // <bench> is a registry name, or file:<prefix> for an authored kernel
 // (<prefix>.ir + <prefix>.gen.json, via the reference's parse_kernel,
@@ -65,6 +70,7 @@ int main(int argc, char** argv) {
     double max_seconds = std::stod(argv[6]);
     int64_t budget = argc > 7 ? std::stoll(argv[7]) : 1000000;
     double tol = argc > 8 ? std::stod(argv[8]) : 0.0;
+    const size_t start = argc > 9 ? std::stoull(argv[9]) : 0;
 
     std::vector<Kernel> variants;
     std::string line;
@@ -73,6 +79,13 @@ int main(int argc, char** argv) {
             continue;
         variants.push_back(apply_patch(kernel, patch_from_json(line)).kernel);
     }
+    // untimed: validation, and the sample order (from `start`, wrapping)
+    std::vector<char> valid(variants.size(), 0);
+    for (size_t i = 0; i < variants.size(); ++i)
+        valid[i] = is_valid(variants[i]);
+    std::vector<size_t> order(variants.size());
+    for (size_t i = 0; i < order.size(); ++i)
+        order[i] = (start + i) % order.size();
     auto tests = registry ? generate_tests(b, n_tests, seed)
                           : generate_tests_for(kernel, gen, n_tests, seed);
     ExecConfig cfg = ExecConfig::for_kernel(kernel);
@@ -97,10 +110,11 @@ int main(int argc, char** argv) {
     for (int w = 0; w < threads; ++w)
         pool.emplace_back([&] {
             for (;;) {
-                size_t i = next.fetch_add(1);
-                if (i >= variants.size() || stop.load())
+                const size_t k = next.fetch_add(1);
+                if (k >= variants.size() || stop.load())
                     return;
-                if (is_valid(variants[i])) {
+                const size_t i = order[k];
+                if (valid[i]) {
                     const EvalOutcome o = evaluate_fitness(variants[i], tests, cfg, tol);
                     ran[i] = o.accepted ? n_suite : o.failing_test + 1;
                 }
@@ -126,7 +140,7 @@ int main(int argc, char** argv) {
             execs += ran[i];
             continue;
         }
-        if (!is_valid(variants[i]))
+        if (!valid[i])
             continue;
         for (const auto& t : tests) {
             ExecResult r = execute(variants[i], t, unit);

@@ -14,6 +14,12 @@
 //   vmcases                    hand-written kernels that exercise every trap class
 //   nsga <n>                   random fitness sets -> rank_population / select_best /
 //                              tournament_select
+//   nsga_bin <in.bin> <keep> <out.bin> [reps]
+//                              one large fitness set (n, then n costs, then n errors,
+//                              native doubles) -> rank_population + select_best; writes
+//                              n_fronts, front[n], crowding[n], fronts flattened, and
+//                              select_best[keep] to out.bin; prints the wall seconds of
+//                              rank_population + select_best (best of reps) as JSON
 //   run <bench> <seed> <pop> <gens> <mode> <train> <heldout> <outdir>
 //                              reference CLI run (log.csv, report.json)
 //   authored <kernel.ir> <gen.json> <n_tests> <seed> <patches.txt> <budget> <tol>
@@ -27,6 +33,7 @@
 
 #include <json.hpp>
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -509,6 +516,47 @@ int cmd_authored(int argc, char** argv) {
     return 0;
 }
 
+int cmd_nsga_bin(int argc, char** argv) {
+    if (argc < 5) {
+        std::cerr << "usage: nsga_bin <in.bin> <keep> <out.bin> [reps]\n";
+        return 1;
+    }
+    std::ifstream in(argv[2], std::ios::binary);
+    int64_t n = 0;
+    in.read(reinterpret_cast<char*>(&n), 8);
+    std::vector<double> c(static_cast<size_t>(n)), e(static_cast<size_t>(n));
+    in.read(reinterpret_cast<char*>(c.data()), n * 8);
+    in.read(reinterpret_cast<char*>(e.data()), n * 8);
+    std::vector<FitnessVector> fits(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i)
+        fits[static_cast<size_t>(i)] = FitnessVector{c[static_cast<size_t>(i)], e[static_cast<size_t>(i)]};
+    const size_t keep = std::stoull(argv[3]);
+    const int reps = argc > 5 ? std::stoi(argv[5]) : 1;
+    double best_s = 1e300, rank_s = 1e300;
+    ParetoRank r;
+    std::vector<int> sel;
+    for (int k = 0; k < reps; ++k) {
+        auto t0 = std::chrono::steady_clock::now();
+        r = rank_population(fits);
+        auto t1 = std::chrono::steady_clock::now();
+        sel = select_best(r, keep);
+        auto t2 = std::chrono::steady_clock::now();
+        best_s = std::min(best_s, std::chrono::duration<double>(t2 - t0).count());
+        rank_s = std::min(rank_s, std::chrono::duration<double>(t1 - t0).count());
+    }
+    std::ofstream out(argv[4], std::ios::binary);
+    const int32_t F = static_cast<int32_t>(r.fronts.size());
+    out.write(reinterpret_cast<const char*>(&F), 4);
+    out.write(reinterpret_cast<const char*>(r.front.data()), n * 4);
+    out.write(reinterpret_cast<const char*>(r.crowding.data()), n * 8);
+    for (const auto& f : r.fronts)
+        out.write(reinterpret_cast<const char*>(f.data()), static_cast<std::streamsize>(f.size() * 4));
+    out.write(reinterpret_cast<const char*>(sel.data()), static_cast<std::streamsize>(sel.size() * 4));
+    std::printf("{\"n\": %lld, \"fronts\": %d, \"rank_select_s\": %.6f, \"rank_s\": %.6f}\n",
+                static_cast<long long>(n), F, best_s, rank_s);
+    return 0;
+}
+
 } // namespace
 
 int main(int argc, char** argv) {
@@ -528,6 +576,8 @@ int main(int argc, char** argv) {
         return cmd_nsga(argc > 2 ? std::stoi(argv[2]) : 200);
     if (cmd == "run")
         return cmd_run(argc, argv);
+    if (cmd == "nsga_bin")
+        return cmd_nsga_bin(argc, argv);
     if (cmd == "authored")
         return cmd_authored(argc, argv);
     std::cerr << "unknown subcommand\n";

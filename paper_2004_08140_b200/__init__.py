@@ -129,6 +129,7 @@ _SIGNATURES = [
     ("gevo_nsga_select", ctypes.c_int, [_vp, _vp, _i32, ctypes.c_int, _i32, _vp, _u64, _i32,
                                         _vp]),
     ("gevo_rank", ctypes.c_int, [_vp, _vp, _i32, ctypes.c_int, _vp, _vp, _vp, _vp, _vp]),
+    ("gevo_select_best", ctypes.c_int, [_vp, _vp, _i32, ctypes.c_int, _i32, _vp, _vp]),
     ("gevo_crowding", ctypes.c_int, [_vp, _vp, _i32, ctypes.c_int, _vp]),
     ("gevo_kernel_canonical", ctypes.c_int, [ctypes.c_char_p, _str_out]),
     ("gevo_kernel_validate", ctypes.c_int, [ctypes.c_char_p, _str_out]),
@@ -489,6 +490,19 @@ def nsga_select(cost, error, keep: int, tournament_seed: int, k: int, device: in
     _check(lib().gevo_nsga_select(vp(c), vp(e), len(c), device, keep, vp(best), tournament_seed,
                                   k, vp(tour)))
     return best[:keep].tolist(), tour[:k].tolist()
+
+
+def select_best(cost, error, keep: int, device: int = -1):
+    """rank_population + select_best(rank, keep) in one device pass:
+    (keep order as int32 array, device ms of the ranking kernels)."""
+    c = np.ascontiguousarray(cost, dtype=np.float64)
+    e = np.ascontiguousarray(error, dtype=np.float64)
+    best = np.zeros(max(keep, 1), np.int32)
+    ms = ctypes.c_float()
+    _check(lib().gevo_select_best(c.ctypes.data_as(ctypes.c_void_p), e.ctypes.data_as(ctypes.c_void_p),
+                                  len(c), device, keep, best.ctypes.data_as(ctypes.c_void_p),
+                                  ctypes.byref(ms)))
+    return best[:keep], ms.value
 
 
 def crowding(cost, error, device: int = -1):

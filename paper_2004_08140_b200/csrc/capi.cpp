@@ -399,17 +399,36 @@ int gevo_nsga_select(const double* cost, const double* error, int32_t n, int dev
         std::vector<FitnessVector> fits(static_cast<size_t>(n));
         for (int32_t i = 0; i < n; ++i)
             fits[static_cast<size_t>(i)] = FitnessVector{cost[i], error[i]};
-        const ParetoRank r = b200::rank_on_device(dev, fits, false);
-        if (best_out) {
-            const std::vector<int> best = select_best(r, static_cast<size_t>(keep));
+        ParetoRank r;
+        const std::vector<int> best =
+            b200::select_on_device(dev, fits, static_cast<size_t>(std::max(keep, 0)), &r);
+        if (best_out)
             std::copy(best.begin(), best.end(), best_out);
-        }
         if (tournament_out) {
             Rng rng(tournament_seed);
             const std::vector<int> t =
                 tournament_select(r, static_cast<size_t>(n), static_cast<size_t>(k), rng);
             std::copy(t.begin(), t.end(), tournament_out);
         }
+    });
+}
+
+int gevo_select_best(const double* cost, const double* error, int32_t n, int device, int32_t keep,
+                     int32_t* best_out, float* device_ms) {
+    return guard([&] {
+        if (n < 0 || keep < 0 || keep > n)
+            throw std::invalid_argument("gevo_select_best: need 0 <= keep <= n");
+        std::unique_ptr<b200::Device> own;
+        b200::Device& dev = device_for(device, own);
+        std::vector<FitnessVector> fits(static_cast<size_t>(n));
+        for (int32_t i = 0; i < n; ++i)
+            fits[static_cast<size_t>(i)] = FitnessVector{cost[i], error[i]};
+        float ms = 0.0f;
+        const std::vector<int> best = b200::select_on_device(dev, fits, static_cast<size_t>(keep), nullptr, &ms);
+        if (best_out)
+            std::copy(best.begin(), best.end(), best_out);
+        if (device_ms)
+            *device_ms = ms;
     });
 }
 

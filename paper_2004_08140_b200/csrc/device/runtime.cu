@@ -83,6 +83,7 @@ struct DeviceImpl {
     cudaStream_t own_stream = nullptr; // created here; `stream` may be a caller's
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     DevBuf blob, counters, rank;
+    gevo::RankWorkspace rws; // GPU rank_population / select_best buffers
     Scratch sc;
     PinnedBuf h_blob, h_vrec, h_rec;
 };
@@ -115,6 +116,7 @@ Device::Device(int ordinal) : impl_(std::make_unique<DeviceImpl>()) {
 }
 
 Device::~Device() {
+    gevo::rank_release(impl_->rws);
     if (impl_->own_stream)
         cudaStreamDestroy(impl_->own_stream);
     cudaEventDestroy(impl_->ev0);
@@ -786,63 +788,88 @@ void spin_counters(Device& devh, uint64_t out[2], bool reset) { read_counters(de
 
 void tp_counters(Device& devh, uint64_t out[2], bool reset) { read_counters(devh, out, reset, 2); }
 
-ParetoRank rank_on_device(Device& devh, const std::vector<FitnessVector>& fits, bool single_group) {
-    ParetoRank r;
+namespace {
+
+// Uploads the fitness vectors and ranks them on the device; with keep >= 0 also
+// computes select_best. Returns the number of fronts; fills `r` when given.
+int32_t rank_impl(Device& devh, const std::vector<FitnessVector>& fits, bool single_group,
+                  int64_t keep, ParetoRank* r, std::vector<int>* best, float* device_ms) {
     const int32_t n = static_cast<int32_t>(fits.size());
-    r.front.assign(fits.size(), -1);
-    r.crowding.assign(fits.size(), 0.0);
+    if (r) {
+        r->front.assign(fits.size(), -1);
+        r->crowding.assign(fits.size(), 0.0);
+        r->fronts.clear();
+    }
+    if (best)
+        best->clear();
     if (n == 0)
-        return r;
+        return 0;
     std::lock_guard<std::mutex> g(devh.lock());
     DeviceImpl& dev = devh.impl();
     check(cudaSetDevice(dev.ordinal), "cudaSetDevice");
     cudaStream_t s = dev.stream;
+    gevo::RankWorkspace& w = dev.rws;
+    check(gevo::rank_reserve(w, n), "rank buffers");
     const size_t N = static_cast<size_t>(n);
-    // layout: cost, err, stair, crowd (double); order, front, offsets(n+1), fill, members,
-    // ord_cost, ord_err, n_fronts (int32)
-    const size_t dbytes = 4 * N * 8, ibytes = (7 * N + 2) * 4;
-    dev.rank.reserve(dbytes + ibytes);
-    char* base = dev.rank.as<char>();
-    gevo::RankBuffers B{};
-    double* dcost = reinterpret_cast<double*>(base);
-    double* derr = dcost + N;
-    B.cost = dcost;
-    B.err = derr;
-    B.stair = derr + N;
-    B.crowd = derr + 2 * N;
-    int32_t* ib = reinterpret_cast<int32_t*>(base + dbytes);
-    B.order = ib;
-    B.front = ib + N;
-    B.offsets = ib + 2 * N;
-    B.fill = ib + 3 * N + 1;
-    B.members = ib + 4 * N + 1;
-    B.ord_cost = ib + 5 * N + 1;
-    B.ord_err = ib + 6 * N + 1;
-    B.n_fronts = ib + 7 * N + 1;
     std::vector<double> hc(N), he(N);
     for (size_t i = 0; i < N; ++i) {
         hc[i] = fits[i].cost;
         he[i] = fits[i].error;
     }
-    check(cudaMemcpyAsync(dcost, hc.data(), N * 8, cudaMemcpyHostToDevice, s), "rank H2D");
-    check(cudaMemcpyAsync(derr, he.data(), N * 8, cudaMemcpyHostToDevice, s), "rank H2D");
-    check(gevo::launch_rank(B, n, single_group, s), "rank kernels");
-    std::vector<int32_t> front(N), members(N), offsets(N + 1);
-    int32_t F = 0;
-    check(cudaMemcpyAsync(front.data(), B.front, N * 4, cudaMemcpyDeviceToHost, s), "rank D2H");
-    check(cudaMemcpyAsync(members.data(), B.members, N * 4, cudaMemcpyDeviceToHost, s), "rank D2H");
-    check(cudaMemcpyAsync(offsets.data(), B.offsets, (N + 1) * 4, cudaMemcpyDeviceToHost, s),
-          "rank D2H");
-    check(cudaMemcpyAsync(r.crowding.data(), B.crowd, N * 8, cudaMemcpyDeviceToHost, s), "rank D2H");
-    check(cudaMemcpyAsync(&F, B.n_fronts, 4, cudaMemcpyDeviceToHost, s), "rank D2H");
+    check(cudaMemcpyAsync(w.cost, hc.data(), N * 8, cudaMemcpyHostToDevice, s), "rank H2D");
+    check(cudaMemcpyAsync(w.err, he.data(), N * 8, cudaMemcpyHostToDevice, s), "rank H2D");
+    check(cudaEventRecord(dev.ev0, s), "event");
+    check(gevo::launch_rank(w, n, single_group, static_cast<int32_t>(keep), s), "rank kernels");
+    check(cudaEventRecord(dev.ev1, s), "event");
+    int32_t meta[gevo::kMetaCount] = {};
+    std::vector<int32_t> front, members, offsets;
+    if (r) {
+        front.resize(N);
+        members.resize(N);
+        offsets.resize(N + 1);
+        check(cudaMemcpyAsync(front.data(), w.front, N * 4, cudaMemcpyDeviceToHost, s), "rank D2H");
+        check(cudaMemcpyAsync(members.data(), w.members, N * 4, cudaMemcpyDeviceToHost, s), "rank D2H");
+        check(cudaMemcpyAsync(offsets.data(), w.offsets, (N + 1) * 4, cudaMemcpyDeviceToHost, s),
+              "rank D2H");
+        check(cudaMemcpyAsync(r->crowding.data(), w.crowd, N * 8, cudaMemcpyDeviceToHost, s), "rank D2H");
+    }
+    if (best && keep > 0) {
+        best->resize(static_cast<size_t>(keep));
+        check(cudaMemcpyAsync(best->data(), w.select, static_cast<size_t>(keep) * 4,
+                              cudaMemcpyDeviceToHost, s),
+              "select D2H");
+    }
+    check(cudaMemcpyAsync(meta, w.meta, sizeof(meta), cudaMemcpyDeviceToHost, s), "rank D2H");
     check(cudaStreamSynchronize(s), "rank");
-    for (size_t i = 0; i < N; ++i)
-        r.front[i] = front[i];
-    r.fronts.resize(static_cast<size_t>(F));
-    for (int32_t f = 0; f < F; ++f)
-        r.fronts[static_cast<size_t>(f)].assign(members.begin() + offsets[static_cast<size_t>(f)],
-                                                members.begin() + offsets[static_cast<size_t>(f) + 1]);
+    if (device_ms)
+        check(cudaEventElapsedTime(device_ms, dev.ev0, dev.ev1), "elapsed");
+    const int32_t F = meta[gevo::kMetaFronts];
+    if (r) {
+        for (size_t i = 0; i < N; ++i)
+            r->front[i] = front[i];
+        r->fronts.resize(static_cast<size_t>(F));
+        for (int32_t f = 0; f < F; ++f)
+            r->fronts[static_cast<size_t>(f)].assign(members.begin() + offsets[static_cast<size_t>(f)],
+                                                     members.begin() + offsets[static_cast<size_t>(f) + 1]);
+    }
+    return F;
+}
+
+} // namespace
+
+ParetoRank rank_on_device(Device& devh, const std::vector<FitnessVector>& fits, bool single_group) {
+    ParetoRank r;
+    rank_impl(devh, fits, single_group, -1, &r, nullptr, nullptr);
     return r;
+}
+
+std::vector<int> select_on_device(Device& devh, const std::vector<FitnessVector>& fits, size_t keep,
+                                  ParetoRank* rank, float* device_ms) {
+    if (keep > fits.size())
+        throw std::invalid_argument("select_best: keep exceeds the population");
+    std::vector<int> best;
+    rank_impl(devh, fits, false, static_cast<int64_t>(keep), rank, &best, device_ms);
+    return best;
 }
 
 double error_on_device(Device& devh, const BufferMap& candidate, const BufferMap& oracle) {

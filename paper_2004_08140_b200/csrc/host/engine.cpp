@@ -739,8 +739,9 @@ void Engine::step_generation() {
     fits.reserve(pool.size());
     for (const auto& ind : pool)
         fits.push_back(*ind.fitness);
-    const ParetoRank pool_rank = rank_population(fits);
-    const std::vector<int> keep = select_best(pool_rank, pop);
+    // rank_population + select_best of the pool in one device pass
+    // (src/engine.cpp:258-262); only the survivor order comes back
+    const std::vector<int> keep = b200::select_on_device(b200::Device::default_device(), fits, pop);
     std::vector<Individual> next;
     next.reserve(pop);
     for (int i : keep)

@@ -119,6 +119,11 @@ const Collective& collective();
 
 // GPU NSGA ranking (front + crowding + fronts in reference order).
 ParetoRank rank_on_device(Device& dev, const std::vector<FitnessVector>& fits, bool single_group);
+// rank_population + select_best(rank, keep) in one device pass (only the keep
+// order comes back unless `rank` is given); device_ms = CUDA-event time of the
+// ranking kernels.
+std::vector<int> select_on_device(Device& dev, const std::vector<FitnessVector>& fits, size_t keep,
+                                  ParetoRank* rank = nullptr, float* device_ms = nullptr);
 
 // compute_error of two host buffer maps, evaluated by the device metric.
 double error_on_device(Device& dev, const BufferMap& candidate, const BufferMap& oracle);

@@ -3,7 +3,7 @@ python scripts/probe_one.py bench:idx [bench:idx ...]"""
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import paper_2004_08140_b200 as gevo  # noqa: E402
 

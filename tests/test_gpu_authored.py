@@ -100,12 +100,15 @@ def test_authored_original_large(gevo, name, scale):
     assert float(got["error"]) == 0.0 == exp["error"]
 
 
-@pytest.mark.parametrize("name", ["svm-rbf", "conv-bn"])
+@pytest.mark.parametrize("name", ["svm-rbf", "conv-bn", "full_svm-rbf", "full_conv-bn"])
 def test_authored_golden_records(gevo, name):
     """Device records and verdicts against the compiled reference's fixture
-    (oracle/gen_golden_authored.py)."""
+    (oracle/gen_golden_authored.py). The full_* fixtures are the BASELINE
+    shapes (a9a X[32561x123] -> K[32561]; CIFAR in[3x32x32] -> out[64x32x32])
+    with 256 mutants + the original, budget 1e6, tolerance 0.01."""
     from conftest import authored_fixture
     head, recs = authored_fixture(name)
+    name = name.replace("full_", "")
     ir, _ = gevo.authored_kernel(name)
     suite = gevo.Suite.from_spec(ir, json.dumps(head["gen"]), head["n_tests"], head["seed"])
     cfg = suite.exec_config().with_(budget=head["budget"])
