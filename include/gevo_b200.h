@@ -85,6 +85,11 @@ int gevo_set_collective(int rank, int world, gevo_allgather_fn fn, void* ctx);
  * read/write conflict, out2[1] = instances run by the thread-parallel kernel. */
 int gevo_tp_counters(uint64_t* out2, int reset);
 void gevo_free(void* p);
+/* Diagnostic: with GEVO_CTA_CLOCK=1 in the environment, the per-CTA timing of
+ * the last thread-parallel evaluation on the default device:
+ * [variant][test] x {globaltimer start ns, end ns, SM id, device IR} for the
+ * first test of each CTA (zeros elsewhere). No reference counterpart. */
+int gevo_debug_cta_clock(uint64_t* out, size_t words, size_t* copied);
 
 /* ---- test suites (uploaded once, resident in HBM) ------------------------
  * Replaces the per-call test handling of evoir::execute / evaluate_fitness

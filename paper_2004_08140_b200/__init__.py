@@ -129,6 +129,7 @@ _SIGNATURES = [
     ("gevo_nsga_select", ctypes.c_int, [_vp, _vp, _i32, ctypes.c_int, _i32, _vp, _u64, _i32,
                                         _vp]),
     ("gevo_rank", ctypes.c_int, [_vp, _vp, _i32, ctypes.c_int, _vp, _vp, _vp, _vp, _vp]),
+    ("gevo_debug_cta_clock", ctypes.c_int, [_vp, ctypes.c_size_t, _vp]),
     ("gevo_select_best", ctypes.c_int, [_vp, _vp, _i32, ctypes.c_int, _i32, _vp, _vp]),
     ("gevo_crowding", ctypes.c_int, [_vp, _vp, _i32, ctypes.c_int, _vp]),
     ("gevo_kernel_canonical", ctypes.c_int, [ctypes.c_char_p, _str_out]),
@@ -490,6 +491,16 @@ def nsga_select(cost, error, keep: int, tournament_seed: int, k: int, device: in
     _check(lib().gevo_nsga_select(vp(c), vp(e), len(c), device, keep, vp(best), tournament_seed,
                                   k, vp(tour)))
     return best[:keep].tolist(), tour[:k].tolist()
+
+
+def debug_cta_clock(n_variants: int, n_tests: int):
+    """Per-CTA timing of the last evaluation (GEVO_CTA_CLOCK=1):
+    [variant, test, 4] uint64 {start ns, end ns, SM, device IR}."""
+    out = np.zeros((n_variants, n_tests, 4), np.uint64)
+    got = ctypes.c_size_t()
+    _check(lib().gevo_debug_cta_clock(out.ctypes.data_as(ctypes.c_void_p), out.size,
+                                      ctypes.byref(got)))
+    return out
 
 
 def select_best(cost, error, keep: int, device: int = -1):

@@ -413,6 +413,14 @@ int gevo_nsga_select(const double* cost, const double* error, int32_t n, int dev
     });
 }
 
+int gevo_debug_cta_clock(uint64_t* out, size_t words, size_t* copied) {
+    return guard([&] {
+        const size_t n = b200::debug_cta_clock(b200::Device::default_device(), out, words);
+        if (copied)
+            *copied = n;
+    });
+}
+
 int gevo_select_best(const double* cost, const double* error, int32_t n, int device, int32_t keep,
                      int32_t* best_out, float* device_ms) {
     return guard([&] {

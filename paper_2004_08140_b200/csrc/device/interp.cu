@@ -55,6 +55,7 @@ extern __shared__ __align__(16) uint2 g_vfs[]; // value files of the CTA's warps
 namespace {
 
 constexpr int kStopRet = 1, kStopSync = 2, kStopTrap = 3, kStopAbort = 4, kStopIdle = 0;
+constexpr int kStopNone = -1; // run_unit: the thread continues
 // Fewest iterations a spin-accelerator jump may cover.
 constexpr int64_t kSpinMinJump = 4;
 // ts_stop encodings (multi-phase kernels)
@@ -158,6 +159,14 @@ __device__ __forceinline__ uint2 lds2(uint32_t a) {
 __device__ __forceinline__ void sts2(uint32_t a, uint32_t x, uint32_t y) {
     asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
 }
+__device__ __forceinline__ uint32_t ldsb(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void stsb(uint32_t a, uint32_t x) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(x) : "memory");
+}
 __device__ __forceinline__ uint32_t lds1(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -184,13 +193,24 @@ __device__ __forceinline__ unsigned long long lds64(uint32_t a) {
 // kM: 0 = sequential lanes, value file in global scratch; 1 = sequential
 // lanes, value file in shared memory; 2 = thread-parallel (one warp per
 // simulated thread, instance memory in shared-memory cells, interp_tp_kernel).
+// Global-cell thread-parallel lanes (256-thread data-parallel kernels) keep a
+// compact value file -- 4-byte payloads and 1-byte tags in separate arrays --
+// so two 256-thread CTAs fit one SM's shared memory.
+#ifndef GEVO_GC_WIDE_VF
+constexpr bool kGcCompactVF = true;
+#else
+constexpr bool kGcCompactVF = false;
+#endif
+
 template <int kM>
 struct Lane {
     static constexpr bool kSmem = kM >= 1;
     static constexpr bool kTP = kM >= 2;
     static constexpr bool kGC = kM == 3; // instance memory cells in global memory
-    uint32_t vsh;    // kSmem: shared address of slot 0
+    static constexpr bool kCompact = kGC && kGcCompactVF;
+    uint32_t vsh;    // kSmem: shared address of slot 0 (kCompact: its payload word)
     uint32_t vstr;   // kSmem: bytes from one slot to the next
+    uint32_t gsh;    // kCompact: shared address of slot 0's tag byte (32 bytes per slot)
     // kTP: only SSA values and phi staging live in the lane's value file; the
     // parameters (per test) and literals (per variant) are CTA-shared tables
     uint32_t nv;     // kTP: n_values (slots below: lane value file)
@@ -251,7 +271,17 @@ struct Lane {
             return lsh + (s - lit_begin) * 8;
         return vsh + (nv + s - stage_base) * vstr;
     }
+    // kCompact: row of a lane-file slot (values, then phi staging)
     __device__ __forceinline__ uint2 V(uint32_t s) const {
+        if (kCompact) {
+            if (!kTpTables)
+                return make_uint2(lds1(vsh + s * 128), ldsb(gsh + s * 32));
+            if (s < nv || s >= stage_base) {
+                const uint32_t row = s < nv ? s : nv + s - stage_base;
+                return make_uint2(lds1(vsh + row * 128), ldsb(gsh + row * 32));
+            }
+            return lds2(s < lit_begin ? tsh + (s - nv) * tstr : lsh + (s - lit_begin) * 8);
+        }
         if (kTP && kTpTables)
             return lds2(tp_addr(s));
         if (kSmem)
@@ -259,6 +289,19 @@ struct Lane {
         return gvf[base + s * row];
     }
     __device__ __forceinline__ void W(uint32_t s, uint32_t payload, uint32_t tag) {
+        if (kCompact) {
+            if (!kTpTables) {
+                sts1(vsh + s * 128, payload);
+                stsb(gsh + s * 32, tag);
+            } else if (s < nv || s >= stage_base) {
+                const uint32_t row = s < nv ? s : nv + s - stage_base;
+                sts1(vsh + row * 128, payload);
+                stsb(gsh + row * 32, tag);
+            } else {
+                sts2(s < lit_begin ? tsh + (s - nv) * tstr : lsh + (s - lit_begin) * 8, payload, tag);
+            }
+            return;
+        }
         if (kTP && kTpTables)
             sts2(tp_addr(s), payload, tag);
         else if (kSmem)
@@ -1449,38 +1492,17 @@ __device__ __forceinline__ bool misc_op(const InterpArgs& A, Lane<kM>& L, const 
     }
 }
 
-// run_to_barrier (vm.cpp:340-387) + step (389-482) for one simulated thread
-// from (th.block, th.ip). Returns kStopRet, kStopSync or kStopTrap.
+// One scheduling unit of a simulated thread at pc: a straight-line run of
+// plain arithmetic, one other instruction, or a branch with the entry of its
+// target block. Returns kStopNone to continue, else the stop kind.
 template <int kM>
-__device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th,
-                          const volatile int32_t* first_fail) {
-    Spin S;
-    S.mode = 0;
-    S.skip = 0;
-    S.attempts = 0;
-    S.next = A.sp_base ? A.spin_threshold : INT64_MAX;
-    S.avoid = -1;
-    S.K = S.H = 0;
-    int64_t bcost;
-    Blk b = load_blk(L.dblk, th.block, bcost);
-    charge_block(A, L, th, b, bcost, static_cast<uint32_t>(th.ip));
-    const uint4* code = reinterpret_cast<const uint4*>(L.code);
-    // pc indexes the variant's records; every block is followed by a
-    // fell-off sentinel record, and the batch array is padded, so the
-    // one-ahead prefetch never leaves it.
-    uint32_t pc = b.start + static_cast<uint32_t>(th.ip);
-#ifdef GEVO_PREFETCH
-    uint4 nxt = __ldg(code + pc);
-#endif
-    for (;;) {
-#ifdef GEVO_PREFETCH
-        uint4 r = nxt;
-        nxt = __ldg(code + pc + 1);
-#else
-        // (a one-ahead prefetch measured slower: the loop-carried copy of the
-        // prefetched record waits for the load anyway)
+__device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread& th, Spin& S, Blk& b,
+                                        uint32_t& pc, const uint4* code,
+                                        const volatile int32_t* first_fail) {
+    {
+        // (a one-ahead prefetch across units measured slower: the loop-carried
+        // copy of the prefetched record waits for the load anyway)
         uint4 r = __ldg(code + pc);
-#endif
         uint32_t op = f_op(r);
         if (th.slow || S.mode == 2) {
             // exact per-instruction charging near the budget / abstract iterate
@@ -1566,9 +1588,6 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
                 if (op > GEVO_OP_FCMP || op == GEVO_OP_SDIV || op == GEVO_OP_FDIV)
                     break;
             }
-#ifdef GEVO_PREFETCH
-            nxt = __ldg(code + pc + 1);
-#endif
         }
 #endif
         bool ok;
@@ -1608,7 +1627,7 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
                 if (res != GEVO_NO_RESULT) {
                     L.W(res, v, vt);
                     ++pc;
-                    continue;
+                    return kStopNone;
                 }
                 L.trap(GEVO_TRAP_DEF_NO_ID);
             } else
@@ -1648,7 +1667,7 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
                 if (ok && res != GEVO_NO_RESULT) {
                     L.W(res, v, vt);
                     ++pc;
-                    continue;
+                    return kStopNone;
                 }
                 if (ok)
                     L.trap(GEVO_TRAP_DEF_NO_ID);
@@ -1709,10 +1728,7 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
             if ((th.executed >= S.next || S.mode != 0) && !th.slow)
                 spin_at_entry(A, L, th, S);
             pc = b.start + static_cast<uint32_t>(th.ip);
-#ifdef GEVO_PREFETCH
-            nxt = __ldg(code + pc);
-#endif
-            continue;
+            return kStopNone;
         } else if (op == GEVO_OP_LOAD || op == GEVO_OP_STORE) {
 #ifndef GEVO_NO_MEM_FAST
             ok = (Lane<kM>::kTP && mem_fast(A, L, r)) || mem_op(A, L, r);
@@ -1742,6 +1758,51 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
             return kStopTrap;
         }
         ++pc;
+        return kStopNone;
+    }
+}
+
+// run_to_barrier (vm.cpp:340-387) + step (389-482) for one simulated thread
+// from (th.block, th.ip). Returns kStopRet, kStopSync or kStopTrap.
+//
+// Reconvergence: the lanes of a warp that run simulated threads together
+// (the same variant) advance in rounds; each round only the lanes at the
+// warp's lowest pc run one unit, the others wait. Blocks are laid out in
+// program order (loop headers before their bodies), so lanes that split at a
+// data-dependent branch meet again at the first block both paths reach, and
+// from there issue the same records together instead of serialising
+// different opcodes every step. Scheduling does not change any result: each
+// lane is an independent simulated thread, and same-phase cross-thread
+// interactions are resolved by the timing-independent rules of the
+// thread-parallel kernel.
+template <int kM>
+__device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thread& th,
+                          const volatile int32_t* first_fail) {
+    Spin S;
+    S.mode = 0;
+    S.skip = 0;
+    S.attempts = 0;
+    S.next = A.sp_base ? A.spin_threshold : INT64_MAX;
+    S.avoid = -1;
+    S.K = S.H = 0;
+    int64_t bcost;
+    Blk b = load_blk(L.dblk, th.block, bcost);
+    charge_block(A, L, th, b, bcost, static_cast<uint32_t>(th.ip));
+    const uint4* code = reinterpret_cast<const uint4*>(L.code);
+    // pc indexes the variant's records; every block is followed by a
+    // fell-off sentinel record, and the batch array is padded, so the
+    // one-ahead prefetch never leaves it.
+    uint32_t pc = b.start + static_cast<uint32_t>(th.ip);
+    const bool gate = A.reconv != 0;
+    unsigned live = __activemask();
+    for (;;) {
+        int stop = kStopNone;
+        if (!gate || pc == __reduce_min_sync(live, pc))
+            stop = run_unit(A, L, th, S, b, pc, code, first_fail);
+        if (gate)
+            live = __ballot_sync(live, stop == kStopNone);
+        if (stop != kStopNone)
+            return stop;
     }
 }
 
@@ -2029,7 +2090,41 @@ enum : uint32_t { kInstPar = 0, kInstSeq = 1, kInstDone = 2 };
 constexpr uint32_t kStickySeq = 2;
 enum : uint32_t { kActContinue = 0, kActFinish = 1, kActRestart = 2, kActNone = 3 };
 
+// Per-CTA scratch regions (InterpArgs::regions): a ring of free region ids
+// with generation tags. Ticket k of the acquire counter takes ring entry
+// k % R once its generation is k / R, i.e. after release k - R returned a
+// region there; at most R CTAs are resident, so that release has been
+// ticketed when ticket k is drawn and the wait is short.
+__device__ uint32_t region_acquire(const InterpArgs& A) {
+    const uint32_t k = atomicAdd(A.region_ctr, 1u);
+    const uint32_t R = A.regions, at = k % R, gen = (k / R) & 0xFFFFu;
+    const volatile uint32_t* q = A.region_q;
+    for (;;) {
+        const uint32_t e = q[at];
+        if ((e >> 16) == gen)
+            return e & 0xFFFFu;
+        __nanosleep(64);
+    }
+}
+
+__device__ void region_release(const InterpArgs& A, uint32_t region) {
+    __threadfence(); // the CTA's scratch writes precede the hand-over
+    const uint32_t k = atomicAdd(A.region_ctr + 1, 1u);
+    const uint32_t R = A.regions, at = k % R, gen = ((k / R) + 1) & 0xFFFFu;
+    *reinterpret_cast<volatile uint32_t*>(A.region_q + at) = region | (gen << 16);
+}
+
+__global__ void region_init_kernel(uint32_t* q, uint32_t* ctr, uint32_t R) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < R; i += gridDim.x * blockDim.x)
+        q[i] = i; // generation 0
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctr[0] = 0;
+        ctr[1] = 0;
+    }
+}
+
 struct TpInst {
+    uint32_t region;
     int32_t min_stop[32];
     uint32_t state[32];
     uint32_t conflict[32];
@@ -2057,6 +2152,10 @@ struct TpGeom {
 template <int kM>
 __device__ __forceinline__ void tp_init_cells(const InterpArgs& A, const Lane<kM>& L, uint32_t tid,
                                               uint32_t T) {
+    if (Lane<kM>::kGC && A.regions)
+        // a reused region: clear the access records of the previous CTA
+        for (uint32_t w = tid; w < A.n_cells; w += T)
+            L.gshadow[static_cast<size_t>(w) * L.gstr] = 0ull;
     const uint32_t SW = static_cast<uint32_t>(max(A.shared_words, 0));
     for (uint32_t w = tid; w < SW; w += T)
         L.cell_put(w, 0, GEVO_TAG_UNDEF);
@@ -2122,7 +2221,10 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
     const uint32_t sbase = smem_addr(g_vfs);
     const uint32_t P = static_cast<uint32_t>(A.n_params);
     const uint32_t lane_slots = kTpTables ? A.lane_slots : A.max_slots;
-    const uint32_t tab0 = sbase + warps * 32 * lane_slots * 8;
+    // compact lane files: [warp][slot][lane] payload words, then tag bytes
+    const uint32_t vf_bytes = Lane<kM>::kCompact ? (warps * 32 * lane_slots * 5 + 7) & ~7u
+                                                 : warps * 32 * lane_slots * 8;
+    const uint32_t tab0 = sbase + vf_bytes;
     const uint32_t lit0 = tab0 + Ln * (P + 2) * 8;
     const uint32_t cell0 = lit0 + A.max_lits * 8;
     const uint32_t smem_cells = kGC ? 0 : A.n_cells;
@@ -2136,8 +2238,15 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
 
     Lane<kM> L;
     L.gvf = nullptr;
-    L.vsh = sbase + (w * 32 * lane_slots + l) * 8;
-    L.vstr = 32 * 8;
+    if (Lane<kM>::kCompact) {
+        L.vsh = sbase + (w * 32 * lane_slots + l) * 4;
+        L.vstr = 32 * 4;
+        L.gsh = sbase + warps * 32 * lane_slots * 4 + w * 32 * lane_slots + l;
+    } else {
+        L.vsh = sbase + (w * 32 * lane_slots + l) * 8;
+        L.vstr = 32 * 8;
+        L.gsh = 0;
+    }
     L.tsh = tab0 + j * 8;
     L.tstr = Ln * 8;
     L.lsh = lit0;
@@ -2175,6 +2284,9 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
     L.n_values = 0;
 
     const volatile int32_t* first_fail = A.first_fail;
+    unsigned long long clk0 = 0;
+    if (A.cta_clock && threadIdx.x == 0)
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(clk0));
     if (threadIdx.x < 32) {
         const uint32_t c = threadIdx.x; // instance column
         const uint32_t tc = tg * Ln + c;
@@ -2203,6 +2315,27 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
         }
     }
     __syncthreads();
+    if (A.regions) {
+        // this CTA's scratch columns (global cells + access records, spin and
+        // snapshot state): a free region, when any of its instances runs
+        if (threadIdx.x == 0) {
+            bool any = false;
+            for (uint32_t c = 0; c < Ln; ++c)
+                any |= S.state[c] != kInstDone;
+            S.region = any ? region_acquire(A) : 0xFFFFFFFFu;
+        }
+        __syncthreads();
+        const uint32_t rg = S.region;
+        if (rg != 0xFFFFFFFFu) {
+            // a region holds its instances' cells contiguously, [cell][test]:
+            // consecutive threads touching consecutive words coalesce
+            const size_t base = static_cast<size_t>(rg) * A.n_cells * Ln + j;
+            L.gcell = kGC ? A.gcells + base : nullptr;
+            L.gshadow = kGC ? A.gshadow + base : nullptr;
+            L.gstr = Ln;
+            L.sl = rg * blockDim.x + threadIdx.x;
+        }
+    }
 
     const gevo_variant var = A.variants[v];
     // CTA-shared tables: the variant's literals, each test's parameters
@@ -2442,6 +2575,17 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
             break;
     }
 
+    if (A.cta_clock && threadIdx.x == 0) {
+        unsigned long long clk1;
+        uint32_t smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(clk1));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        unsigned long long* c = A.cta_clock + (static_cast<size_t>(v) * nt + tg * Ln) * 4;
+        c[0] = clk0;
+        c[1] = clk1;
+        c[2] = smid;
+        c[3] = S.ir[0];
+    }
     // compute_error (src/vm.cpp:536-556) of completed instances: max over
     // oracle elements, spread over the instance's threads (max is order-free).
     double worst = 0.0;
@@ -2468,6 +2612,8 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
     if (lane_ok)
         errs[q] = worst;
     __syncthreads();
+    if (A.regions && threadIdx.x == 0 && S.region != 0xFFFFFFFFu)
+        region_release(A, S.region);
     if (!leader || !inst_ok)
         return;
     double error = -1.0;
@@ -2697,11 +2843,13 @@ cudaError_t launch_interp(const InterpArgs& A, cudaStream_t stream) {
 }
 
 size_t tp_smem_bytes(uint32_t threads, uint32_t lanes, const TpTables& tab, uint32_t n_cells,
-                     uint32_t n_chunks, bool backup) {
+                     uint32_t n_chunks, bool backup, bool gc) {
     const uint32_t K = 32 / lanes;
     const size_t warps = (threads + K - 1) / K;
     const size_t Q = static_cast<size_t>(threads) * lanes;
-    size_t b = warps * 32 * (kTpTables ? tab.lane_slots : tab.max_slots) * 8 +
+    const size_t vf = warps * 32 * (kTpTables ? tab.lane_slots : tab.max_slots);
+    const bool compact = gc && kGcCompactVF;
+    size_t b = (compact ? (vf * 5 + 7) & ~size_t(7) : vf * 8) +
                (static_cast<size_t>(lanes) * (tab.n_params + 2) + tab.max_lits) * 8 +
                static_cast<size_t>(lanes) * n_cells * 8 * (backup ? 2 : 1) +
                2 * static_cast<size_t>(n_chunks) * warps * 32 * 4 + 4 * Q * 4;
@@ -2709,7 +2857,7 @@ size_t tp_smem_bytes(uint32_t threads, uint32_t lanes, const TpTables& tab, uint
 }
 
 TpShape tp_shape(uint32_t threads, uint32_t n_tests, const TpTables& tab, uint32_t n_cells,
-                 uint32_t n_chunks, bool backup) {
+                 uint32_t n_chunks, bool backup, bool gc) {
     TpShape s{0, 0, 0};
     if (threads < 1 || threads > kTpMaxBlock)
         return s;
@@ -2719,12 +2867,16 @@ TpShape tp_shape(uint32_t threads, uint32_t n_tests, const TpTables& tab, uint32
         const char* e = std::getenv("GEVO_TP_LANES"); // tests per CTA upper bound (tuning)
         return e ? static_cast<uint32_t>(std::max(1, std::min(32, std::atoi(e)))) : 32u;
     }();
-    for (uint32_t ln = min(max(n_tests, 1u), cap); ln >= 1; --ln) {
+    // kernels of a warp or more of threads fill whole warps with one test per
+    // CTA: no lanes of a later test run speculatively beside an earlier
+    // test's, and the early-exit protocol skips the later tests' CTAs
+    const uint32_t top = threads >= 32 ? 1u : min(max(n_tests, 1u), cap);
+    for (uint32_t ln = top; ln >= 1; --ln) {
         const uint32_t K = 32 / ln;
         const uint32_t warps = (threads + K - 1) / K;
         if (warps * 32 > kTpMaxBlock)
             continue;
-        const size_t bytes = tp_smem_bytes(threads, ln, tab, n_cells, n_chunks, backup);
+        const size_t bytes = tp_smem_bytes(threads, ln, tab, n_cells, n_chunks, backup, gc);
         if (bytes <= kSmemBudget) {
             s.warps_per_cta = warps;
             s.lanes = ln;
@@ -2735,13 +2887,24 @@ TpShape tp_shape(uint32_t threads, uint32_t n_tests, const TpTables& tab, uint32
     return s;
 }
 
+uint32_t tp_resident_ctas(bool global_cells, uint32_t warps_per_cta, size_t smem) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const void* fn = global_cells ? reinterpret_cast<const void*>(interp_tp_kernel<3>)
+                                  : reinterpret_cast<const void*>(interp_tp_kernel<2>);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, static_cast<int>(32 * warps_per_cta), smem);
+    return static_cast<uint32_t>(std::max(per_sm, 1) * std::max(sms, 1));
+}
+
 cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream) {
     if (A.n_inst == 0)
         return cudaSuccess;
     const bool gc = A.gcells != nullptr;
     const TpShape s = tp_shape(static_cast<uint32_t>(A.threads), static_cast<uint32_t>(A.n_tests),
                                TpTables{A.lane_slots, A.max_slots, static_cast<uint32_t>(A.n_params), A.max_lits},
-                               gc ? 0 : A.n_cells, gc ? 0 : A.n_chunks, A.tp_snap != nullptr);
+                               gc ? 0 : A.n_cells, gc ? 0 : A.n_chunks, A.tp_snap != nullptr, gc);
     if (s.warps_per_cta == 0 || s.lanes != A.tp_lanes)
         return cudaErrorInvalidConfiguration;
     const unsigned grid = A.n_var * ((static_cast<uint32_t>(A.n_tests) + s.lanes - 1) / s.lanes);
@@ -2753,6 +2916,9 @@ cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream) {
         cudaFuncSetAttribute(interp_tp_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
         cudaFuncSetAttribute(interp_tp_kernel<3>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
     }
+    if (A.regions)
+        region_init_kernel<<<(A.regions + 255) / 256, 256, 0, stream>>>(A.region_q, A.region_ctr,
+                                                                       A.regions);
     if (gc) {
         const cudaError_t e = cudaFuncSetAttribute(
             interp_tp_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(s.smem));

@@ -112,6 +112,17 @@ struct InterpArgs {
     int32_t early_exit;
     uint64_t* counters;             // [4]: accelerated spins, jumped instructions,
                                     // tp instances re-run in id order, tp instances (nullable)
+    // thread-parallel per-CTA scratch regions: a CTA takes a free region of
+    // the global cells / access records / spin and snapshot columns when it
+    // starts and returns it when it ends, so scratch is sized by the CTAs
+    // that can be resident, not by the batch (0: one column set per instance)
+    uint32_t regions;
+    uint32_t* region_q;             // [regions] free-region ring: region | generation << 16
+    uint32_t* region_ctr;           // [2] acquire / release tickets
+    uint32_t reconv;                // run_thread reconvergence gate (lanes of one test)
+    unsigned long long* cta_clock;  // diagnostic (nullable): [variant][test] x 4 for the first
+                                    // test of each thread-parallel CTA: globaltimer at CTA
+                                    // start and end, SM id, device IR of the CTA
 };
 
 // Memory words one abstract iterate may store to / load from.
@@ -159,8 +170,11 @@ struct TpTables {
     uint32_t max_lits;
 };
 TpShape tp_shape(uint32_t threads, uint32_t n_tests, const TpTables& tab, uint32_t n_cells,
-                 uint32_t n_chunks, bool backup);
+                 uint32_t n_chunks, bool backup, bool gc = false);
 cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream);
+// CTAs of the thread-parallel kernel that can be resident at once for shape
+// (warps, smem) on this device (the region count of a launch).
+uint32_t tp_resident_ctas(bool global_cells, uint32_t warps_per_cta, size_t smem);
 cudaError_t launch_error(const uint32_t* cand, const uint32_t* orc, const uint8_t* elem, uint32_t n,
                          double* out, cudaStream_t stream);
 cudaError_t launch_fitness(const gevo_test_record* rec, uint32_t n_variants, int32_t n_tests,

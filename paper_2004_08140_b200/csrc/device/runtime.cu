@@ -74,7 +74,14 @@ struct Scratch {
     DevBuf ts_pos, ts_prev, ts_exec, ts_stop, ts_val, ts_tag;
     DevBuf tp_snap, gcells, gshadow, outcells, suffix, sp_vk;
     DevBuf bcost, vf, sp_base, sp_btag, sp_delta, sp_cur, sp_hvary, sp_cvary, sp_log, sp_ld;
-    size_t scratch_budget = size_t(8) << 30; // bytes of per-instance scratch per launch
+    // bytes of per-instance scratch per launch (GEVO_SCRATCH_GB); larger
+    // batches run in several launches
+    size_t scratch_budget = [] {
+        const char* e = std::getenv("GEVO_SCRATCH_GB");
+        return (e ? static_cast<size_t>(std::max(1, std::atoi(e))) : size_t(8)) << 30;
+    }();
+    DevBuf cta_clock; // diagnostic per-CTA timing (GEVO_CTA_CLOCK=1)
+    DevBuf regions;   // thread-parallel region ring + tickets
 };
 
 struct DeviceImpl {
@@ -267,6 +274,44 @@ bool tp_enabled() {
     return v;
 }
 
+// GEVO_CTA_CLOCK=1: the thread-parallel kernel records per-CTA timing.
+bool cta_clock_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("GEVO_CTA_CLOCK");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+struct CtaClockRef {
+    const DevBuf* buf = nullptr;
+    size_t bytes = 0;
+};
+CtaClockRef& last_cta_clock() {
+    static CtaClockRef r;
+    return r;
+}
+
+// GEVO_RECONV=0/1 forces the reconvergence gate off/on; by default it is on
+// when the lanes of a warp are threads of one test.
+int reconv_mode() {
+    static const int v = [] {
+        const char* e = std::getenv("GEVO_RECONV");
+        return e ? (e[0] == '0' ? 0 : 1) : -1;
+    }();
+    return v;
+}
+
+// GEVO_TP_REGIONS=0 gives every instance its own scratch columns (one
+// launch per scratch budget) instead of the per-CTA region pool.
+bool regions_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("GEVO_TP_REGIONS");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 // Spin-accelerator scratch for `cols` columns (instances or lanes).
 void reserve_spin(Scratch& sc, gevo::InterpArgs& A, size_t cols) {
     const size_t n = cols * A.max_slots;
@@ -337,6 +382,14 @@ int launch_all(DeviceImpl& dev, Scratch& sc, DeviceSuite& suite, gevo::InterpArg
         check(cudaMemsetAsync(dev.counters.ptr, 0, 32, s), "counters");
     }
     A.counters = dev.counters.as<uint64_t>();
+    A.cta_clock = nullptr;
+    if (cta_clock_enabled()) {
+        const size_t bytes = std::max<size_t>(static_cast<size_t>(h.n_variants) * T * 32, 32);
+        sc.cta_clock.reserve(bytes);
+        check(cudaMemsetAsync(sc.cta_clock.ptr, 0, bytes, s), "cta clock");
+        A.cta_clock = sc.cta_clock.as<unsigned long long>();
+        last_cta_clock() = {&sc.cta_clock, bytes};
+    }
 
     // Thread-parallel lanes (one lane per simulated thread) whenever the
     // instance state fits on chip; the sequential-lane kernel otherwise.
@@ -353,7 +406,7 @@ int launch_all(DeviceImpl& dev, Scratch& sc, DeviceSuite& suite, gevo::InterpArg
     gevo::TpShape tps = gevo::tp_shape(threads, T, tab, n_cells, n_chunks, h.any_sync != 0);
     bool gc = false;
     if (tps.warps_per_cta == 0) {
-        tps = gevo::tp_shape(threads, T, tab, 0, 0, false);
+        tps = gevo::tp_shape(threads, T, tab, 0, 0, false, true);
         gc = tps.warps_per_cta > 0;
     }
     if (ex.threads >= 1 && !opt.sequential && tps.warps_per_cta > 0 && tp_enabled()) {
@@ -361,6 +414,8 @@ int launch_all(DeviceImpl& dev, Scratch& sc, DeviceSuite& suite, gevo::InterpArg
         const uint32_t tgroups = (T + tps.lanes - 1) / tps.lanes;
         A.n_cells = n_cells;
         A.n_chunks = n_chunks;
+        A.reconv = reconv_mode() >= 0 ? static_cast<uint32_t>(reconv_mode())
+                                      : static_cast<uint32_t>(tps.lanes == 1);
         const size_t per_lane = thr > 0 ? 15 * static_cast<size_t>(A.max_slots) + 28 * gevo::kSpinLog
                                         : 0;
         const size_t lanes_per_variant = static_cast<size_t>(tgroups) * 32 * tps.warps_per_cta;
@@ -371,7 +426,19 @@ int launch_all(DeviceImpl& dev, Scratch& sc, DeviceSuite& suite, gevo::InterpArg
         chunk = std::min<size_t>(chunk, std::max<uint32_t>(h.n_variants, 1));
         if (opt.want_outputs)
             chunk = std::max<uint32_t>(h.n_variants, 1); // one launch window
-        const size_t lanes = chunk * lanes_per_variant;
+        // per-CTA regions: scratch for the CTAs that can be resident, one
+        // launch for the whole batch (outputs read back per instance keep
+        // the per-instance layout)
+        A.regions = 0;
+        if (gc && regions_enabled() && !opt.want_outputs) {
+            A.regions = gevo::tp_resident_ctas(gc, tps.warps_per_cta, tps.smem);
+            chunk = std::max<uint32_t>(h.n_variants, 1);
+            sc.regions.reserve((static_cast<size_t>(A.regions) + 2) * 4);
+            A.region_ctr = sc.regions.as<uint32_t>();
+            A.region_q = A.region_ctr + 2;
+        }
+        const size_t lanes = A.regions ? static_cast<size_t>(A.regions) * 32 * tps.warps_per_cta
+                                       : chunk * lanes_per_variant;
         if (thr > 0) {
             reserve_spin(sc, A, lanes);
             A.spin_threshold = thr;
@@ -381,7 +448,8 @@ int launch_all(DeviceImpl& dev, Scratch& sc, DeviceSuite& suite, gevo::InterpArg
         A.gcells = nullptr;
         A.gshadow = nullptr;
         if (gc) {
-            const size_t cells = std::max<size_t>(static_cast<size_t>(n_cells) * chunk * T, 1);
+            const size_t cols = A.regions ? static_cast<size_t>(A.regions) * tps.lanes : chunk * T;
+            const size_t cells = std::max<size_t>(static_cast<size_t>(n_cells) * cols, 1);
             sc.gcells.reserve(cells * 8);
             sc.gshadow.reserve(cells * 8);
             A.gcells = sc.gcells.as<uint2>();
@@ -407,8 +475,8 @@ int launch_all(DeviceImpl& dev, Scratch& sc, DeviceSuite& suite, gevo::InterpArg
             L.v_begin = static_cast<uint32_t>(vb);
             L.n_var = static_cast<uint32_t>(std::min<uint64_t>(chunk, h.n_variants - vb));
             L.n_inst = L.n_var * T;
-            L.n_spin = static_cast<uint32_t>(L.n_var * lanes_per_variant);
-            if (gc)
+            L.n_spin = static_cast<uint32_t>(A.regions ? lanes : L.n_var * lanes_per_variant);
+            if (gc && !A.regions) // (regions clear their records when taken)
                 check(cudaMemsetAsync(A.gshadow, 0,
                                       static_cast<size_t>(n_cells) * L.n_inst * 8, s),
                       "access records");
@@ -870,6 +938,20 @@ std::vector<int> select_on_device(Device& devh, const std::vector<FitnessVector>
     std::vector<int> best;
     rank_impl(devh, fits, false, static_cast<int64_t>(keep), rank, &best, device_ms);
     return best;
+}
+
+size_t debug_cta_clock(Device& devh, uint64_t* out, size_t words) {
+    std::lock_guard<std::mutex> g(devh.lock());
+    DeviceImpl& dev = devh.impl();
+    const CtaClockRef r = last_cta_clock();
+    if (!r.buf || !r.buf->ptr)
+        return 0;
+    const size_t n = std::min(words, r.bytes / 8);
+    check(cudaSetDevice(dev.ordinal), "cudaSetDevice");
+    check(cudaStreamSynchronize(dev.stream), "cta clock");
+    check(cudaDeviceSynchronize(), "cta clock");
+    check(cudaMemcpy(out, r.buf->ptr, n * 8, cudaMemcpyDeviceToHost), "cta clock D2H");
+    return n;
 }
 
 double error_on_device(Device& devh, const BufferMap& candidate, const BufferMap& oracle) {

@@ -125,6 +125,11 @@ ParetoRank rank_on_device(Device& dev, const std::vector<FitnessVector>& fits, b
 std::vector<int> select_on_device(Device& dev, const std::vector<FitnessVector>& fits, size_t keep,
                                   ParetoRank* rank = nullptr, float* device_ms = nullptr);
 
+// Diagnostic: per-CTA timing of the last thread-parallel evaluation with
+// GEVO_CTA_CLOCK=1 ([variant][test] x {start ns, end ns, SM, device IR});
+// returns the words copied.
+size_t debug_cta_clock(Device& dev, uint64_t* out, size_t words);
+
 // compute_error of two host buffer maps, evaluated by the device metric.
 double error_on_device(Device& dev, const BufferMap& candidate, const BufferMap& oracle);
 

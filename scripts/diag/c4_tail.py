@@ -1,13 +1,15 @@
 """GPU probe: what sets the config-4 step time. Evaluates the bench's
-config-4 batch with per-test records, splits the variants by the status of
-their first test (completed / trap / budget) and times each class alone as
-its own resident batch; prints one JSON line per class."""
+config-4 batch with per-test records and per-CTA timing (GEVO_CTA_CLOCK=1),
+then prints: the step makespan, SM-time by the class of the variant's first
+test (completed / trap / budget) and of the CTA's role (the test the reference
+runs, or a speculative later test), and the longest CTAs."""
 import gzip
 import json
 import os
 import sys
 
-import numpy as np
+os.environ.setdefault("GEVO_CTA_CLOCK", "1")
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
@@ -22,28 +24,38 @@ cfg = suite.exec_config()
 b = suite.batch()
 for c in cands:
     b.add_patch(c)
+b.eval(cfg, tolerance=0.01, early_exit=True)
 gevo.spin_counters(reset=True)
 v, t, st = b.eval(cfg, tolerance=0.01, early_exit=True, tests=True)
-print(json.dumps({"all": len(cands), "ms": st.device_ms, "spins": gevo.spin_counters(reset=True)}))
+clk = gevo.debug_cta_clock(len(cands), 3).astype(np.int64)
+ran = clk[:, :, 0] > 0
+t0 = clk[:, :, 0][ran].min()
+dur = (clk[:, :, 1] - clk[:, :, 0]) / 1e6  # ms
+end = (clk[:, :, 1] - t0) / 1e6
+print(json.dumps({"variants": len(cands), "device_ms": st.device_ms, "launches": st.launches,
+                  "makespan_ms": float(end[ran].max()), "ctas": int(ran.sum()),
+                  "sm_ms_total": float(dur[ran].sum()), "spins": gevo.spin_counters(reset=True)}))
 s0 = t["status"][:, 0]
+ff = v["failing_test"]
 for name, cls in (("completed", 0), ("trap", 1), ("budget", 2)):
-    idx = np.nonzero(s0 == cls)[0]
-    if len(idx) == 0:
+    rows = s0 == cls
+    for role in ("reference", "speculative"):
+        m = np.zeros_like(ran)
+        for tt in range(3):
+            ref_run = (ff < 0) | (ff >= tt)
+            m[:, tt] = rows & ran[:, tt] & (ref_run if role == "reference" else ~ref_run)
+        if m.sum() == 0:
+            continue
+        print(json.dumps({"class": name, "role": role, "ctas": int(m.sum()),
+                          "sm_ms": float(dur[m].sum()), "max_ms": float(dur[m].max()),
+                          "mean_ms": float(dur[m].mean()),
+                          "ir_mean": float(clk[:, :, 3][m].mean())}))
+order = np.argsort(-dur, axis=None)[:12]
+for k in order:
+    vi, ti = divmod(int(k), 3)
+    if not ran[vi, ti]:
         continue
-    bb = suite.batch()
-    for i in idx:
-        bb.add_patch(cands[i])
-    bb.make_resident()
-    bb.eval_resident(cfg, tolerance=0.01, early_exit=True)
-    _, st2 = bb.eval_resident(cfg, tolerance=0.01, early_exit=True)
-    irs = t["ir"][idx, 0]
-    print(json.dumps({"class": name, "variants": int(len(idx)), "ms": st2.device_ms,
-                      "ir_test0_mean": float(irs.mean()), "ir_test0_max": int(irs.max()),
-                      "jumps": int(t["pad"][idx, 0, 0].sum()) if t["pad"].ndim == 3 else None}))
-# slowest single variants of the budget class, alone
-idx = np.nonzero(s0 == 2)[0][:8]
-for i in idx:
-    bb = suite.batch().add_patch(cands[i])
-    _, _, st3 = bb.eval(cfg, tolerance=0.01, early_exit=True)
-    print(json.dumps({"budget_variant": int(i), "ms": st3.device_ms, "ir": int(t["ir"][i, 0]),
-                      "cost": int(t["cost"][i, 0]), "patch": cands[i][:300]}))
+    print(json.dumps({"cta": [vi, ti], "ms": float(dur[vi, ti]), "end_ms": float(end[vi, ti]),
+                      "status": int(t["status"][vi, ti]), "code": int(t["code"][vi, ti]),
+                      "ir": int(t["ir"][vi, ti]), "cta_ir": int(clk[vi, ti, 3]),
+                      "jumps": int(t["pad"][vi, ti, 0]), "patch": cands[vi][:200]}))

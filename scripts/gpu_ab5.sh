@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+for e in "GEVO_RECONV=1" "GEVO_RECONV=0"; do
+  echo "== $e"
+  env $e timeout 900 python scripts/diag/c4_tail.py 4096 2>&1 | head -1 | cut -c1-250
+  env $e timeout 600 python scripts/bench_configs.py config3 --steps 2 --cpu-seconds 0 2>&1 | tail -1 | cut -c1-120
+done
+GEVO_TRACE=1 timeout 1200 python scripts/search_time.py --ref > gpurun_out/search_time.log 2>&1; tail -12 gpurun_out/search_time.log | cut -c1-400
