@@ -189,6 +189,7 @@ int gevo_select_best(const double* cost, const double* error, int32_t n, int dev
 /* ---- host-side API of the search (no device work) ------------------------ */
 int gevo_kernel_canonical(const char* kernel_ir, char** printed);          /* parse + print */
 int gevo_kernel_validate(const char* kernel_ir, char** rules_json);        /* validate() */
+int gevo_kernel_is_valid(const char* kernel_ir, int32_t* valid);           /* is_valid() */
 int gevo_apply_patch(const char* kernel_ir, const char* patch_json, char** printed,
                      int32_t* n_applied);                                   /* apply_patch */
 /* random_mutation (src/operators.cpp:348) on `kernel_ir` with

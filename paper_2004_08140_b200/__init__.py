@@ -134,6 +134,7 @@ _SIGNATURES = [
     ("gevo_crowding", ctypes.c_int, [_vp, _vp, _i32, ctypes.c_int, _vp]),
     ("gevo_kernel_canonical", ctypes.c_int, [ctypes.c_char_p, _str_out]),
     ("gevo_kernel_validate", ctypes.c_int, [ctypes.c_char_p, _str_out]),
+    ("gevo_kernel_is_valid", ctypes.c_int, [ctypes.c_char_p, _vp]),
     ("gevo_apply_patch", ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, _str_out,
                                         ctypes.POINTER(_i32)]),
     ("gevo_random_mutation", ctypes.c_int, [ctypes.c_char_p, _u64, _u64, _u64, _u64, _str_out,
@@ -211,6 +212,13 @@ def validate(ir: str) -> list:
     out = ctypes.c_void_p()
     _check(lib().gevo_kernel_validate(_b(ir), ctypes.byref(out)))
     return json.loads(_take(out))
+
+
+def is_valid(ir: str) -> bool:
+    """is_valid (ir.hpp:258): validate(k).empty() by the verdict-only path."""
+    v = ctypes.c_int32()
+    _check(lib().gevo_kernel_is_valid(_b(ir), ctypes.byref(v)))
+    return bool(v.value)
 
 
 def apply_patch(ir: str, patch) -> tuple:

@@ -511,6 +511,10 @@ int gevo_kernel_validate(const char* kernel_ir, char** rules_json) {
     });
 }
 
+int gevo_kernel_is_valid(const char* kernel_ir, int32_t* valid) {
+    return guard([&] { *valid = is_valid(parse_kernel(kernel_ir)) ? 1 : 0; });
+}
+
 int gevo_apply_patch(const char* kernel_ir, const char* patch_json, char** printed,
                      int32_t* n_applied) {
     return guard([&] {

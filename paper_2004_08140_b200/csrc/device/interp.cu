@@ -1498,7 +1498,7 @@ __device__ __forceinline__ bool misc_op(const InterpArgs& A, Lane<kM>& L, const 
 template <int kM>
 __device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread& th, Spin& S, Blk& b,
                                         uint32_t& pc, const uint4* code,
-                                        const volatile int32_t* first_fail) {
+                                        const volatile int32_t* first_fail, bool& entered) {
     {
         // (a one-ahead prefetch across units measured slower: the loop-carried
         // copy of the prefetched record waits for the load anyway)
@@ -1728,6 +1728,7 @@ __device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread
             if ((th.executed >= S.next || S.mode != 0) && !th.slow)
                 spin_at_entry(A, L, th, S);
             pc = b.start + static_cast<uint32_t>(th.ip);
+            entered = true;
             return kStopNone;
         } else if (op == GEVO_OP_LOAD || op == GEVO_OP_STORE) {
 #ifndef GEVO_NO_MEM_FAST
@@ -1793,13 +1794,41 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
     // fell-off sentinel record, and the batch array is padded, so the
     // one-ahead prefetch never leaves it.
     uint32_t pc = b.start + static_cast<uint32_t>(th.ip);
-    const bool gate = A.reconv != 0;
+    // Adaptive gate: warps run ungated (every lane a whole block per round)
+    // and probe for divergence every 16 rounds; a diverged warp is gated --
+    // only the lanes at the lead pc run, one unit per round, or a whole block
+    // when every lane is at the lead -- until it has stayed converged for 16
+    // rounds. Converged code (data-parallel loops) thus pays a vote per block
+    // and a probe now and then; divergent code reconverges.
+    const bool adapt = A.reconv != 0;
     unsigned live = __activemask();
+    bool gated = false;
+    uint32_t streak = 0;
     for (;;) {
         int stop = kStopNone;
-        if (!gate || pc == __reduce_min_sync(live, pc))
-            stop = run_unit(A, L, th, S, b, pc, code, first_fail);
-        if (gate)
+        bool run = true, together = true;
+        if (adapt) {
+            if (!gated && ++streak >= 16) {
+                streak = 0;
+                gated = __reduce_min_sync(live, pc) != __reduce_max_sync(live, pc);
+            }
+            if (gated) {
+                run = pc == __reduce_min_sync(live, pc);
+                together = __all_sync(live, run);
+                streak = together ? streak + 1 : 0;
+                if (streak >= 16) {
+                    gated = false;
+                    streak = 0;
+                }
+            }
+        }
+        if (run) {
+            bool entered = false;
+            do
+                stop = run_unit(A, L, th, S, b, pc, code, first_fail, entered);
+            while (together && stop == kStopNone && !entered);
+        }
+        if (adapt)
             live = __ballot_sync(live, stop == kStopNone);
         if (stop != kStopNone)
             return stop;

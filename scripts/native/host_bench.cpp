@@ -1,7 +1,9 @@
 // Host candidate-production microbenchmark (no GPU): per-call cost of the
 // pieces the search engine runs for every attempt -- random_mutation,
 // apply_edit, apply_patch (crossover children are re-applied from the
-// original), is_valid, Kernel copy. Build:
+// original), is_valid, Kernel copy -- plus two equivalence checks: in-place
+// apply_patch == the apply_edit fold, and the verdict-only is_valid ==
+// validate().empty() on unfiltered (mostly invalid) children. Build:
 //   g++ -O2 -std=c++20 -Iinclude scripts/native/host_bench.cpp \
 //       -Lpaper_2004_08140_b200 -lgevo_b200 -Wl,-rpath,$PWD/paper_2004_08140_b200 -o /tmp/host_bench
 #include "evoir/corpus.hpp"
@@ -77,6 +79,38 @@ int main(int argc, char** argv) {
     std::printf("apply_patch vs apply_edit fold: %zu patches, %zu dropped edits, %zu mismatches\n",
                 checked, dropped, mism);
     if (mism)
+        return 1;
+    // verdict-only is_valid == validate().empty() on unfiltered children:
+    // random mutations of every walk kernel and the crossover children (most
+    // of them invalid, across every rule)
+    size_t vchecked = 0, vmism = 0, vinvalid = 0;
+    auto vcheck = [&](const Kernel& k) {
+        const bool full = validate(k).empty();
+        ++vchecked;
+        vinvalid += !full;
+        if (is_valid(k) != full)
+            ++vmism;
+    };
+    for (size_t i = 0; i < kernels.size(); ++i) {
+        const DomTree dom = DomTree::build(kernels[i]);
+        MutationContext ctx(kernels[i], dom, rng);
+        for (int j = 0; j < 12; ++j) {
+            MutationResult m = random_mutation(ctx);
+            if (!m)
+                continue;
+            ApplyResult ap = apply_edit(kernels[i], *m);
+            if (ap.applied)
+                vcheck(ap.kernel);
+        }
+        if (i + 1 < patches.size()) {
+            auto [ca, cb] = crossover_messy(patches[i], patches[i + 1], rng);
+            vcheck(apply_patch(b.kernel, ca).kernel);
+            vcheck(apply_patch(b.kernel, cb).kernel);
+        }
+    }
+    std::printf("is_valid vs validate: %zu kernels (%zu invalid), %zu validity mismatches\n", vchecked,
+                vinvalid, vmism);
+    if (vmism)
         return 1;
     auto t = clk::now();
     for (auto& p : patches)

@@ -2,7 +2,9 @@
 compiled against include/evoir and libgevo_b200.so and checks that the
 in-place apply_patch equals the left fold of apply_edit (the reference's
 definition, src/genome.cpp:216-227) on random walks and on their messy
-crossover children (many edits no longer apply), for every corpus kernel."""
+crossover children (many edits no longer apply), for every corpus kernel, and
+that the verdict-only is_valid equals validate().empty() on thousands of
+unfiltered (mostly invalid) mutation and crossover children."""
 import os
 import subprocess
 
@@ -29,3 +31,4 @@ def test_in_place_apply_patch_equals_edit_fold(host_bench, bench):
     out = subprocess.run([host_bench, bench, "16"], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert " 0 mismatches" in out.stdout, out.stdout
+    assert " 0 validity mismatches" in out.stdout, out.stdout
