@@ -80,6 +80,16 @@ int gevo_spin_counters(uint64_t* out2, int reset);
  * is single-process. */
 typedef void (*gevo_allgather_fn)(void* ctx, const void* send, size_t bytes, void* recv);
 int gevo_set_collective(int rank, int world, gevo_allgather_fn fn, void* ctx);
+/* In-library multi-GPU exchange (one process per GPU): the engine's record
+ * all-gather runs as ncclAllGather on the device buffers of the evaluation
+ * (NVLink / NVSwitch), no host staging. One rank calls gevo_nccl_unique_id
+ * (128 bytes) and distributes it; every rank then calls gevo_set_nccl with
+ * its rank and the world size (world <= 0 leaves the communicator). Takes
+ * precedence over gevo_set_collective. Shards are contiguous and cut at equal
+ * shares of the predicted cost (the parents' mean cost). No reference
+ * counterpart (src/engine.cpp:28-62 is single-process). */
+int gevo_nccl_unique_id(void* out128);
+int gevo_set_nccl(int rank, int world, const void* id128);
 /* Thread-parallel interpreter counters since the last reset: out2[0] =
  * instances re-executed in thread-id order after a same-phase cross-thread
  * read/write conflict, out2[1] = instances run by the thread-parallel kernel. */

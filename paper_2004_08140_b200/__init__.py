@@ -96,6 +96,8 @@ _SIGNATURES = [
     ("gevo_set_stream", ctypes.c_int, [_vp]),
     ("gevo_spin_counters", ctypes.c_int, [_vp, ctypes.c_int]),
     ("gevo_tp_counters", ctypes.c_int, [_vp, ctypes.c_int]),
+    ("gevo_nccl_unique_id", ctypes.c_int, [_vp]),
+    ("gevo_set_nccl", ctypes.c_int, [ctypes.c_int, ctypes.c_int, _vp]),
     ("gevo_set_collective", ctypes.c_int, [ctypes.c_int, ctypes.c_int, _vp, _vp]),
     ("gevo_free", None, [_vp]),
     ("gevo_suite_from_benchmark", ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _u64, ctypes.c_int,

@@ -157,6 +157,14 @@ int gevo_set_collective(int rank, int world, gevo_allgather_fn fn, void* ctx) {
     });
 }
 
+int gevo_nccl_unique_id(void* out128) {
+    return guard([&] { b200::nccl_unique_id(out128); });
+}
+
+int gevo_set_nccl(int rank, int world, const void* id128) {
+    return guard([&] { b200::set_nccl(rank, world, id128); });
+}
+
 int gevo_tp_counters(uint64_t* out2, int reset) {
     return guard([&] { b200::tp_counters(b200::Device::default_device(), out2, reset != 0); });
 }

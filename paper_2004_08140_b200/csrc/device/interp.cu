@@ -1794,33 +1794,19 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
     // fell-off sentinel record, and the batch array is padded, so the
     // one-ahead prefetch never leaves it.
     uint32_t pc = b.start + static_cast<uint32_t>(th.ip);
-    // Adaptive gate: warps run ungated (every lane a whole block per round)
-    // and probe for divergence every 16 rounds; a diverged warp is gated --
-    // only the lanes at the lead pc run, one unit per round, or a whole block
-    // when every lane is at the lead -- until it has stayed converged for 16
-    // rounds. Converged code (data-parallel loops) thus pays a vote per block
-    // and a probe now and then; divergent code reconverges.
-    const bool adapt = A.reconv != 0;
+    // When every live lane is at the lead pc the warp is converged and stays
+    // so until a branch: it runs units up to the next block entry before the
+    // next gate (one gate per block, not per unit, on converged code).
+    // (An adaptive variant -- ungated until a periodic probe sees divergence
+    // -- measured slower on both configs 3 and 4.)
+    const bool gate = A.reconv != 0;
     unsigned live = __activemask();
-    bool gated = false;
-    uint32_t streak = 0;
     for (;;) {
         int stop = kStopNone;
         bool run = true, together = true;
-        if (adapt) {
-            if (!gated && ++streak >= 16) {
-                streak = 0;
-                gated = __reduce_min_sync(live, pc) != __reduce_max_sync(live, pc);
-            }
-            if (gated) {
-                run = pc == __reduce_min_sync(live, pc);
-                together = __all_sync(live, run);
-                streak = together ? streak + 1 : 0;
-                if (streak >= 16) {
-                    gated = false;
-                    streak = 0;
-                }
-            }
+        if (gate) {
+            run = pc == __reduce_min_sync(live, pc);
+            together = __all_sync(live, run);
         }
         if (run) {
             bool entered = false;
@@ -1828,7 +1814,7 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
                 stop = run_unit(A, L, th, S, b, pc, code, first_fail, entered);
             while (together && stop == kStopNone && !entered);
         }
-        if (adapt)
+        if (gate)
             live = __ballot_sync(live, stop == kStopNone);
         if (stop != kStopNone)
             return stop;

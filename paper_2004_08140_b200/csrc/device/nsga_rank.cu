@@ -382,6 +382,213 @@ __global__ void select_kernel(const int32_t* __restrict__ members, const int32_t
         out[q] = q < seg[0] ? members[q] : sorted[q];
 }
 
+// ---- small pools: the whole ranking in one CTA ---------------------------
+//
+// For pools of up to kSmallN members (a search ranks pools of 1.25 x pop
+// every generation) the multi-kernel pipeline above is launch-bound. Here one
+// CTA does everything in shared memory with O(n^2 / 1024) counting passes:
+// lexicographic positions, fronts by the staircase (one warp), ascending-index
+// members, per-front cost / error positions, crowding and select_best.
+constexpr int kSmallN = 2048;
+constexpr int kSmallThreads = 1024;
+
+__device__ __forceinline__ bool lex_less(double a0, double b0, int32_t i0, double a1, double b1,
+                                         int32_t i1) {
+    if (a0 != a1)
+        return a0 < a1;
+    if (b0 != b1)
+        return b0 < b1;
+    return i0 < i1;
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    rank_small_kernel(const double* __restrict__ gcost, const double* __restrict__ gerr, int32_t n,
+                      bool single_group, int32_t keep, int32_t* __restrict__ front_out,
+                      int32_t* __restrict__ members_out, int32_t* __restrict__ offsets_out,
+                      double* __restrict__ crowd_out, int32_t* __restrict__ select_out,
+                      int32_t* __restrict__ meta) {
+    extern __shared__ double sm[];
+    double* cost = sm;
+    double* err = sm + n;
+    int32_t* A = reinterpret_cast<int32_t*>(sm + 2 * n); // A order: index at each position
+    int32_t* B = A + n;        // B order
+    int32_t* posA = B + n;     // position of each index in A
+    int32_t* posB = posA + n;
+    int32_t* front = posB + n;
+    int32_t* off = front + n;  // [n + 1] front offsets
+    int32_t* ocost = off + n + 1;
+    int32_t* oerr = ocost + n;
+    int32_t* stair = oerr + n;
+    __shared__ int32_t sF, sCut;
+    const int tid = threadIdx.x;
+    for (int32_t i = tid; i < n; i += kSmallThreads) {
+        cost[i] = gcost[i];
+        err[i] = gerr[i];
+    }
+    __syncthreads();
+    // 1. lexicographic positions (cost, error, index) and (error, cost, index)
+    for (int32_t i = tid; i < n; i += kSmallThreads) {
+        const double ci = cost[i], ei = err[i];
+        int32_t pa = 0, pb = 0;
+        for (int32_t j = 0; j < n; ++j) {
+            const double cj = cost[j], ej = err[j];
+            pa += lex_less(cj, ej, j, ci, ei, i);
+            pb += lex_less(ej, cj, j, ei, ci, i);
+        }
+        posA[i] = pa;
+        posB[i] = pb;
+        A[pa] = i;
+        B[pb] = i;
+    }
+    __syncthreads();
+    // 2. fronts: the staircase over the A order (identical points share a
+    //    front), one warp, 32-ary search of the staircase
+    if (tid < 32) {
+        const int lane = tid;
+        int32_t F = 0, last = -1;
+        if (single_group) {
+            for (int32_t p = lane; p < n; p += 32)
+                front[A[p]] = 0;
+            F = 1;
+        } else {
+            for (int32_t p = 0; p < n; ++p) {
+                const int32_t i = A[p];
+                const double c = cost[i], e = err[i];
+                if (p > 0 && c == cost[A[p - 1]] && e == err[A[p - 1]]) {
+                    if (lane == 0)
+                        front[i] = last;
+                    continue;
+                }
+                int32_t lo = 0, hi = F;
+                while (hi - lo > 32) {
+                    const int32_t step = (hi - lo + 31) >> 5;
+                    const int32_t x = lo + (lane + 1) * step - 1;
+                    const bool le = x < hi && err[stair[x]] <= e;
+                    const int32_t cnt = __popc(__ballot_sync(0xffffffffu, le));
+                    const int32_t nlo = lo + cnt * step;
+                    hi = min(hi, lo + (cnt + 1) * step - 1);
+                    lo = nlo;
+                }
+                const int32_t x = lo + lane;
+                const bool le = x < hi && err[stair[x]] <= e;
+                const int32_t r = lo + __popc(__ballot_sync(0xffffffffu, le));
+                if (lane == 0) {
+                    stair[r] = i; // (the staircase holds the index of its minimum)
+                    front[i] = r;
+                }
+                __syncwarp();
+                if (r == F)
+                    ++F;
+                last = r;
+            }
+        }
+        if (lane == 0)
+            sF = F;
+    }
+    __syncthreads();
+    const int32_t F = sF;
+    // 3. front sizes -> offsets (count, then a serial prefix over F <= n)
+    for (int32_t f = tid; f <= n; f += kSmallThreads)
+        off[f] = 0;
+    __syncthreads();
+    for (int32_t i = tid; i < n; i += kSmallThreads)
+        atomicAdd(&off[front[i] + 1], 1);
+    __syncthreads();
+    if (tid == 0)
+        for (int32_t f = 1; f <= F; ++f)
+            off[f] += off[f - 1];
+    __syncthreads();
+    // 4. members (ascending index per front) and per-front positions in the
+    //    cost / error orders
+    for (int32_t i = tid; i < n; i += kSmallThreads) {
+        const int32_t f = front[i];
+        int32_t pm = 0, pc = 0, pe = 0;
+        for (int32_t j = 0; j < n; ++j) {
+            if (front[j] != f)
+                continue;
+            pm += j < i;
+            pc += posA[j] < posA[i];
+            pe += posB[j] < posB[i];
+        }
+        members_out[off[f] + pm] = i;
+        ocost[off[f] + pc] = i;
+        oerr[off[f] + pe] = i;
+    }
+    __syncthreads();
+    // posA / posB now: each member's slot in its front's cost / error order
+    for (int32_t q = tid; q < n; q += kSmallThreads) {
+        posA[ocost[q]] = q;
+        posB[oerr[q]] = q;
+    }
+    __syncthreads();
+    // 5. crowding (nsga.cpp:48-86), cost objective first
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    for (int32_t i = tid; i < n; i += kSmallThreads) {
+        const int32_t f = front[i], b = off[f], m = off[f + 1] - b;
+        double d = 0.0;
+        if (m <= 2) {
+            d = inf;
+        } else {
+            const int32_t q1 = posA[i], p1 = q1 - b;
+            const double lo1 = cost[ocost[b]], hi1 = cost[ocost[b + m - 1]];
+            if (p1 == 0 || p1 == m - 1)
+                d = inf;
+            else if (hi1 > lo1)
+                d = __dadd_rn(d, __ddiv_rn(__dsub_rn(cost[ocost[q1 + 1]], cost[ocost[q1 - 1]]),
+                                           __dsub_rn(hi1, lo1)));
+            const int32_t q2 = posB[i], p2 = q2 - b;
+            const double lo2 = err[oerr[b]], hi2 = err[oerr[b + m - 1]];
+            if (p2 == 0 || p2 == m - 1)
+                d = inf;
+            else if (hi2 > lo2 && d != inf)
+                d = __dadd_rn(d, __ddiv_rn(__dsub_rn(err[oerr[q2 + 1]], err[oerr[q2 - 1]]),
+                                           __dsub_rn(hi2, lo2)));
+        }
+        crowd_out[i] = d;
+        front_out[i] = f;
+    }
+    for (int32_t f = tid; f <= F; f += kSmallThreads)
+        offsets_out[f] = off[f];
+    // 6. select_best(keep): whole fronts in ascending index order, the cut
+    //    front by (crowding desc, index asc) (nsga.cpp:126-148)
+    if (keep >= 0) {
+        if (tid == 0) {
+            int32_t c = 0;
+            while (c < F && off[c + 1] <= keep)
+                ++c;
+            sCut = c;
+        }
+        __syncthreads();
+        const int32_t c = sCut;
+        const int32_t b = c < F ? off[c] : off[F];
+        for (int32_t q = tid; q < min(b, keep); q += kSmallThreads)
+            select_out[q] = members_out[q];
+        __syncthreads(); // crowd_out / members_out visible to the block
+        if (c < F) {
+            const int32_t e = off[c + 1];
+            for (int32_t q = b + tid; q < e; q += kSmallThreads) {
+                const int32_t i = members_out[q];
+                const double di = crowd_out[i];
+                int32_t r = 0;
+                for (int32_t u = b; u < e; ++u) {
+                    const int32_t j = members_out[u];
+                    const double dj = crowd_out[j];
+                    r += dj > di || (dj == di && j < i);
+                }
+                if (b + r < keep)
+                    select_out[b + r] = i;
+            }
+        }
+        if (tid == 0)
+            meta[kMetaCut] = c;
+    }
+    if (tid == 0) {
+        meta[kMetaFronts] = F;
+        meta[kMetaGroups] = meta[kMetaCosts] = meta[kMetaErrors] = 0; // (not computed here)
+        meta[kMetaStrategy] = single_group ? 3 : 4; // 4: small-pool single-CTA path
+    }
+}
+
 int bits_for(int32_t n) {
     int b = 1;
     while ((1ll << b) <= n)
@@ -472,6 +679,16 @@ cudaError_t rank_reserve(RankWorkspace& w, int32_t n) {
 cudaError_t launch_rank(RankWorkspace& w, int32_t n, bool single_group, int32_t keep, cudaStream_t s) {
     if (n <= 0) {
         return cudaMemsetAsync(w.meta, 0, kMetaCount * sizeof(int32_t), s);
+    }
+    if (n <= kSmallN) {
+        const size_t smem = static_cast<size_t>(n) * 16 + (static_cast<size_t>(n) * 9 + 1) * 4;
+        cudaError_t e = cudaFuncSetAttribute(rank_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess)
+            return e;
+        rank_small_kernel<<<1, kSmallThreads, smem, s>>>(w.cost, w.err, n, single_group, keep, w.front,
+                                                         w.members, w.offsets, w.crowd, w.select, w.meta);
+        return cudaGetLastError();
     }
     const int grid = (n + kThreads - 1) / kThreads;
     size_t tb = w.cub_bytes;

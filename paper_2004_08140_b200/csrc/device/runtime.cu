@@ -6,6 +6,8 @@
 #include "nsga_rank.cuh"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h> // types only: the library is opened at run time (see nccl_api)
 
 #include <algorithm>
 #include <cstdlib>
@@ -65,6 +67,40 @@ struct PinnedBuf {
 
 } // namespace
 
+namespace {
+// NCCL entry points, resolved when a communicator is first wanted: the copy
+// already in the process (e.g. the one torch loaded) when there is one, else
+// GEVO_NCCL_LIB or the system libnccl.so.2. Not linked at build time, so a
+// process never ends up with two NCCL builds under one soname.
+struct NcclApi {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+};
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) {
+            const char* e = std::getenv("GEVO_NCCL_LIB");
+            h = dlopen(e ? e : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        }
+        if (!h)
+            throw std::runtime_error(std::string("NCCL not found: ") + dlerror());
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        if (!a.get_unique_id || !a.comm_init_rank || !a.all_gather || !a.comm_destroy)
+            throw std::runtime_error("NCCL library lacks an entry point");
+        return a;
+    }();
+    return api;
+}
+} // namespace
+
 // Device scratch of one evaluation stream: records, per-instance memory,
 // spin-accelerator state. The device owns one (synchronous calls); every
 // resident batch owns another, so batches can be evaluated concurrently on
@@ -91,6 +127,9 @@ struct DeviceImpl {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     DevBuf blob, counters, rank;
     gevo::RankWorkspace rws; // GPU rank_population / select_best buffers
+    ncclComm_t nccl = nullptr; // record exchange of a multi-GPU search
+    int nccl_rank = 0, nccl_world = 0;
+    DevBuf gathered;           // all-gathered variant records
     Scratch sc;
     PinnedBuf h_blob, h_vrec, h_rec;
 };
@@ -124,6 +163,7 @@ Device::Device(int ordinal) : impl_(std::make_unique<DeviceImpl>()) {
 
 Device::~Device() {
     gevo::rank_release(impl_->rws);
+    // (a communicator still set at exit is left to the process teardown)
     if (impl_->own_stream)
         cudaStreamDestroy(impl_->own_stream);
     cudaEventDestroy(impl_->ev0);
@@ -611,12 +651,34 @@ EvalResult evaluate(DeviceSuite& suite, BatchImage& batch, const ExecImage& exec
     R.launches = launch_all(dev, dev.sc, suite, A, h, wr, exec, opt, s, &ow);
     check(cudaEventRecord(dev.ev2, s), "event");
 
-    R.variants.resize(h.n_variants);
-    if (h.n_variants) {
-        check(cudaMemcpyAsync(R.variants.data(), dev.sc.vrec.ptr,
-                              h.n_variants * sizeof(gevo_variant_record), cudaMemcpyDeviceToHost, s),
+    if (opt.gather_count > 0 && dev.nccl) {
+        // device-resident exchange: this rank's records (padded to the
+        // largest shard) are all-gathered over NVLink by NCCL, then one D2H
+        const size_t rb = sizeof(gevo_variant_record), m = opt.gather_count;
+        if (h.n_variants > m)
+            throw std::logic_error("shard larger than gather_count");
+        dev.sc.vrec.reserve(m * rb);
+        if (m > h.n_variants)
+            check(cudaMemsetAsync(dev.sc.vrec.as<char>() + h.n_variants * rb, 0,
+                                  (m - h.n_variants) * rb, s),
+                  "gather pad");
+        const size_t W = static_cast<size_t>(dev.nccl_world);
+        dev.gathered.reserve(W * m * rb);
+        if (nccl_api().all_gather(dev.sc.vrec.ptr, dev.gathered.ptr, m * rb, ncclUint8, dev.nccl, s) !=
+            ncclSuccess)
+            throw std::runtime_error("ncclAllGather of the variant records failed");
+        R.variants.resize(W * m);
+        check(cudaMemcpyAsync(R.variants.data(), dev.gathered.ptr, W * m * rb, cudaMemcpyDeviceToHost, s),
               "records D2H");
-        R.d2h_bytes += h.n_variants * sizeof(gevo_variant_record);
+        R.d2h_bytes += W * m * rb;
+    } else {
+        R.variants.resize(h.n_variants);
+        if (h.n_variants) {
+            check(cudaMemcpyAsync(R.variants.data(), dev.sc.vrec.ptr,
+                                  h.n_variants * sizeof(gevo_variant_record), cudaMemcpyDeviceToHost, s),
+                  "records D2H");
+            R.d2h_bytes += h.n_variants * sizeof(gevo_variant_record);
+        }
     }
     const size_t total = static_cast<size_t>(h.n_variants) * S.n_tests;
     if (opt.want_tests || opt.want_outputs) {
@@ -939,6 +1001,42 @@ std::vector<int> select_on_device(Device& devh, const std::vector<FitnessVector>
     rank_impl(devh, fits, false, static_cast<int64_t>(keep), rank, &best, device_ms);
     return best;
 }
+
+
+void nccl_unique_id(void* out128) {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    if (nccl_api().get_unique_id(&id) != ncclSuccess)
+        throw std::runtime_error("ncclGetUniqueId failed");
+    std::memcpy(out128, &id, sizeof(id));
+}
+
+void set_nccl(int rank, int world, const void* id128) {
+    Device& devh = Device::default_device();
+    std::lock_guard<std::mutex> g(devh.lock());
+    DeviceImpl& dev = devh.impl();
+    check(cudaSetDevice(dev.ordinal), "cudaSetDevice");
+    if (dev.nccl) {
+        nccl_api().comm_destroy(dev.nccl);
+        dev.nccl = nullptr;
+        dev.nccl_world = 0;
+    }
+    if (world <= 0)
+        return;
+    if (rank < 0 || rank >= world || !id128)
+        throw std::invalid_argument("set_nccl: need 0 <= rank < world and a unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    if (nccl_api().comm_init_rank(&dev.nccl, world, id, rank) != ncclSuccess) {
+        dev.nccl = nullptr;
+        throw std::runtime_error("ncclCommInitRank failed");
+    }
+    dev.nccl_rank = rank;
+    dev.nccl_world = world;
+}
+
+int nccl_world() { return Device::default_device().impl().nccl_world; }
+int nccl_rank() { return Device::default_device().impl().nccl_rank; }
 
 size_t debug_cta_clock(Device& devh, uint64_t* out, size_t words) {
     std::lock_guard<std::mutex> g(devh.lock());

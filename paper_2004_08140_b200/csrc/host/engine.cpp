@@ -202,7 +202,8 @@ int wave_size(int used, int retries) {
 // [begin_r, end_r) of the batch and the records are all-gathered.
 std::vector<EvalOutcome> device_verdicts(b200::DeviceSuite& suite, const b200::ExecImage& ex,
                                          const std::vector<const Kernel*>& ks, double tol,
-                                         bool with_reasons, EngineCounters& ctr, int jobs = 1) {
+                                         bool with_reasons, EngineCounters& ctr, int jobs = 1,
+                                         const std::vector<double>* weight = nullptr) {
     std::vector<EvalOutcome> out(ks.size());
     if (ks.empty())
         return out;
@@ -215,15 +216,40 @@ std::vector<EvalOutcome> device_verdicts(b200::DeviceSuite& suite, const b200::E
             o = EvalOutcome::rejected(-1, "no test cases");
         return out;
     }
+    // Sharding: with an NCCL communicator in the library (one process per
+    // GPU) the records are all-gathered on the device inside the evaluation;
+    // otherwise through the caller's collective callback (host buffers).
     const b200::Collective& col = b200::collective();
-    const bool shard = col.world > 1 && col.allgather && !with_reasons;
-    const size_t n = ks.size(), W = shard ? static_cast<size_t>(col.world) : 1;
-    const size_t R = shard ? static_cast<size_t>(col.rank) : 0;
-    auto span = [&](size_t r) {
-        const size_t q = n / W, m = n % W;
-        const size_t b = r * q + std::min(r, m);
-        return std::make_pair(b, b + q + (r < m ? 1 : 0));
-    };
+    const int nw = b200::nccl_world();
+    const bool via_nccl = nw >= 1 && !with_reasons;
+    const bool shard = via_nccl || (col.world > 1 && col.allgather && !with_reasons);
+    const size_t n = ks.size();
+    const size_t W = !shard ? 1 : via_nccl ? static_cast<size_t>(nw) : static_cast<size_t>(col.world);
+    const size_t R = !shard ? 0 : via_nccl ? static_cast<size_t>(b200::nccl_rank()) : static_cast<size_t>(col.rank);
+    // contiguous shards (gathered records concatenate back into batch order),
+    // cut at equal shares of the predicted cost when weights are given -- a
+    // budget spinner costs ~10^3 ordinary variants -- else at
+    // equal counts; every rank computes the same cuts
+    std::vector<size_t> cut(W + 1, n);
+    cut[0] = 0;
+    if (weight && weight->size() == n && W > 1) {
+        double total = 0;
+        for (double w : *weight)
+            total += std::max(w, 1.0);
+        double acc = 0;
+        size_t r = 1;
+        for (size_t v = 0; v < n && r < W; ++v) {
+            acc += std::max((*weight)[v], 1.0);
+            while (r < W && acc >= total * static_cast<double>(r) / static_cast<double>(W))
+                cut[r++] = v + 1;
+        }
+    } else {
+        for (size_t r = 1; r < W; ++r) {
+            const size_t q = n / W, m = n % W;
+            cut[r] = r * q + std::min(r, m);
+        }
+    }
+    auto span = [&](size_t r) { return std::make_pair(cut[r], cut[r + 1]); };
     const auto [lo, hi] = span(R);
     // encode in parallel parts (the device bytecode of ~10^5 candidates per
     // search is otherwise a serial host term), joined in candidate order
@@ -249,14 +275,27 @@ std::vector<EvalOutcome> device_verdicts(b200::DeviceSuite& suite, const b200::E
     b200::EvalOptions opt;
     opt.tolerance = tol;
     opt.early_exit = true;
+    size_t m = 0; // largest shard: the exchange pads every shard to it
+    for (size_t q = 0; q < W; ++q)
+        m = std::max(m, cut[q + 1] - cut[q]);
     b200::EvalResult r;
     const auto t_ev = std::chrono::steady_clock::now();
-    if (hi > lo)
+    if (via_nccl) {
+        opt.gather_count = std::max<size_t>(m, 1);
+        r = b200::evaluate(suite, batch, ex, opt); // (an empty shard still joins the all-gather)
+    } else if (hi > lo) {
         r = b200::evaluate(suite, batch, ex, opt);
+    }
     Trace::get().eval_ms += ms_since(t_ev);
     std::vector<gevo_variant_record> recs;
-    if (shard) {
-        const size_t m = (n + W - 1) / W;
+    if (via_nccl) {
+        const size_t mm = std::max<size_t>(m, 1);
+        recs.reserve(n);
+        for (size_t q = 0; q < W; ++q) {
+            const auto [b, e] = span(q);
+            recs.insert(recs.end(), r.variants.begin() + q * mm, r.variants.begin() + q * mm + (e - b));
+        }
+    } else if (shard) {
         std::vector<gevo_variant_record> send(m), recv(m * W);
         std::copy(r.variants.begin(), r.variants.end(), send.begin());
         col.allgather(col.ctx, send.data(), m * sizeof(gevo_variant_record), recv.data());
@@ -433,16 +472,18 @@ void Engine::run_mutations(std::vector<MutJob>& jobs) const {
         });
         // 2. one device batch for every candidate of every slot
         std::vector<const Kernel*> ks;
+        std::vector<double> weight; // predicted cost: the parent's mean cost
         for (MutJob* j : active)
             for (auto& at : j->wave)
                 if (at.candidate) {
                     at.verdict = static_cast<int>(ks.size());
                     ks.push_back(&at.kernel);
+                    weight.push_back(j->parent->fitness ? j->parent->fitness->cost : 1.0);
                 }
         counters_.host_gen_ms += ms_since(t0);
         Trace::get().mut_gen_ms += ms_since(t0);
-        const auto verdicts =
-            device_verdicts(*suite_, *exec_img_, ks, cfg_.tolerance, false, counters_, cfg_.jobs);
+        const auto verdicts = device_verdicts(*suite_, *exec_img_, ks, cfg_.tolerance, false, counters_,
+                                              cfg_.jobs, &weight);
         const auto t_res = std::chrono::steady_clock::now();
         // 3. resolve each slot in attempt order
         for (MutJob* j : active) {
@@ -511,22 +552,29 @@ void Engine::run_crossovers(std::vector<CxJob>& jobs) const {
             }
         });
         std::vector<const Kernel*> ks;
-        for (size_t i = 0; i < active.size(); ++i)
+        std::vector<double> weight; // predicted cost: the parents' mean cost
+        for (size_t i = 0; i < active.size(); ++i) {
+            const CxJob& j = *active[i];
+            const double w = (j.a->fitness ? j.a->fitness->cost : 1.0) / 2 +
+                             (j.b->fitness ? j.b->fitness->cost : 1.0) / 2;
             for (size_t a = 0; a < active[i]->wave.size(); ++a) {
                 auto& at = active[i]->wave[a];
                 if (valid[i][2 * a]) {
                     at.va = static_cast<int>(ks.size());
                     ks.push_back(&at.pa.kernel);
+                    weight.push_back(w);
                 }
                 if (valid[i][2 * a + 1]) {
                     at.vb = static_cast<int>(ks.size());
                     ks.push_back(&at.pb.kernel);
+                    weight.push_back(w);
                 }
             }
+        }
         counters_.host_gen_ms += ms_since(t0);
         Trace::get().cx_gen_ms += ms_since(t0);
-        const auto verdicts =
-            device_verdicts(*suite_, *exec_img_, ks, cfg_.tolerance, false, counters_, cfg_.jobs);
+        const auto verdicts = device_verdicts(*suite_, *exec_img_, ks, cfg_.tolerance, false, counters_,
+                                              cfg_.jobs, &weight);
         const auto t_res = std::chrono::steady_clock::now();
         for (CxJob* j : active) {
             for (auto& at : j->wave) {

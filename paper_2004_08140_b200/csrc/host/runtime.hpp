@@ -58,6 +58,12 @@ struct EvalOptions {
     bool want_tests = false;      // copy per-test records back
     bool want_outputs = false;    // copy final global buffers back (small batches)
     bool sequential = false;      // force the sequential-lane interpreter
+    // Multi-GPU exchange inside the evaluation: with an NCCL communicator on
+    // the device (set_nccl) and gather_count > 0, the batch is this rank's
+    // shard and its variant records (padded to gather_count) are all-gathered
+    // on the device by ncclAllGather; EvalResult::variants then holds
+    // world * gather_count records in rank order.
+    size_t gather_count = 0;
 };
 
 struct EvalResult {
@@ -116,6 +122,15 @@ struct Collective {
 };
 void set_collective(const Collective& c);
 const Collective& collective();
+
+// NCCL communicator of the default device for the in-library record
+// exchange (one process per GPU). nccl_unique_id fills 128 bytes on one
+// rank, which the caller distributes; set_nccl(rank, world, id) joins the
+// communicator (world <= 0 releases it). nccl_world() is 0 without one.
+void nccl_unique_id(void* out128);
+void set_nccl(int rank, int world, const void* id128);
+int nccl_world();
+int nccl_rank();
 
 // GPU NSGA ranking (front + crowding + fronts in reference order).
 ParetoRank rank_on_device(Device& dev, const std::vector<FitnessVector>& fits, bool single_group);

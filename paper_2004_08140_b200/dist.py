@@ -111,6 +111,31 @@ def install_collective(device=None, group=None):
                                      None))
 
 
+def install_nccl(group=None):
+    """In-library exchange: the engine all-gathers its records with its own
+    NCCL communicator on the device buffers of each evaluation (one process
+    per GPU; rank 0's NCCL unique id is broadcast over `group`)."""
+    import ctypes
+
+    import torch.distributed as dist
+
+    from . import lib, _check
+
+    uid = ctypes.create_string_buffer(128)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if rank == 0:
+        _check(lib().gevo_nccl_unique_id(uid))
+    box = [bytes(uid.raw)]
+    dist.broadcast_object_list(box, src=0, group=group)
+    ctypes.memmove(uid, box[0], 128)
+    _check(lib().gevo_set_nccl(rank, world, uid))
+
+
+def uninstall_nccl():
+    from . import lib, _check
+    _check(lib().gevo_set_nccl(0, 0, None))
+
+
 def uninstall_collective():
     from . import lib, _check
     _check(lib().gevo_set_collective(0, 1, None, None))
