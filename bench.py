@@ -281,11 +281,15 @@ def roofline_of(workload, step_ms, f_mhz, ir_ref_step, ir_dev_step):
                 "lanes_per_warp_inst": (prof["thread_inst"] / prof["warp_inst"])
                 if prof.get("thread_inst") else None,
                 "ncu_ms_per_step": prof.get("ncu_ms")})
-    # share of the issued work the reference would also execute (speculative
-    # tests after a variant's first failure are discarded)
+    # device-executed (interpreted) instructions per issued warp instruction,
+    # and the issue fraction scaled to the reference-equivalent work: the
+    # reference runs ir_ref instructions for this step, the device
+    # interpreted ir_dev (jumps make it smaller, discarded speculative work
+    # larger)
     if ir_dev_step:
-        out["useful_ir_fraction"] = ir_ref_step / ir_dev_step
-        out["useful_frac"] = out["frac"] * out["useful_ir_fraction"]
+        out["interpreted_ir_per_step"] = ir_dev_step
+        out["warp_inst_per_interpreted_ir"] = prof["warp_inst"] / ir_dev_step
+        out["reference_ir_per_interpreted_ir"] = ir_ref_step / ir_dev_step
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         hbm_peak, src = peaks["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs"
@@ -367,10 +371,13 @@ def b200_arm(args):
     # untimed pass with per-test records: reference-equivalent and
     # device-executed work of one step
     gevo.spin_counters(reset=True)
+    gevo.work_counters(reset=True)
     v, t, _ = batch.eval(cfg, tolerance=C4["tol"], early_exit=True, tests=True)
     execs_step = int(v["execs_ref"].sum())
     ir_ref_step = int(v["ir_ref"].sum())
-    ir_dev_step = int(t["ir"][t["status"] != 3].sum())
+    # instructions the device actually interpreted in the step: spin jumps
+    # excluded, speculative tests / aborted threads / re-runs included
+    ir_dev_step = gevo.work_counters(reset=True)
     spins = gevo.spin_counters(reset=True)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 

@@ -94,6 +94,12 @@ int gevo_set_nccl(int rank, int world, const void* id128);
  * instances re-executed in thread-id order after a same-phase cross-thread
  * read/write conflict, out2[1] = instances run by the thread-parallel kernel. */
 int gevo_tp_counters(uint64_t* out2, int reset);
+/* Interpreted instructions on the default device since the last reset:
+ * out2[0] = IR instructions the interpreters executed (spin-accelerator jumps
+ * excluded; discarded re-run attempts and aborted threads included), out2[1]
+ * reserved. Device-executed work beside the records' reference-equivalent
+ * counts. */
+int gevo_work_counters(uint64_t* out2, int reset);
 void gevo_free(void* p);
 /* Diagnostic: with GEVO_CTA_CLOCK=1 in the environment, the per-CTA timing of
  * the last thread-parallel evaluation on the default device:

@@ -96,6 +96,7 @@ _SIGNATURES = [
     ("gevo_set_stream", ctypes.c_int, [_vp]),
     ("gevo_spin_counters", ctypes.c_int, [_vp, ctypes.c_int]),
     ("gevo_tp_counters", ctypes.c_int, [_vp, ctypes.c_int]),
+    ("gevo_work_counters", ctypes.c_int, [_vp, ctypes.c_int]),
     ("gevo_nccl_unique_id", ctypes.c_int, [_vp]),
     ("gevo_set_nccl", ctypes.c_int, [ctypes.c_int, ctypes.c_int, _vp]),
     ("gevo_set_collective", ctypes.c_int, [ctypes.c_int, ctypes.c_int, _vp, _vp]),
@@ -300,6 +301,14 @@ def tp_counters(reset: bool = False) -> tuple:
     out = (ctypes.c_uint64 * 2)()
     _check(lib().gevo_tp_counters(ctypes.cast(out, ctypes.c_void_p), 1 if reset else 0))
     return out[0], out[1]
+
+
+def work_counters(reset: bool = False) -> int:
+    """IR instructions the device interpreted since the last reset (jumps
+    excluded, discarded work included)."""
+    out = (ctypes.c_uint64 * 2)()
+    _check(lib().gevo_work_counters(out, 1 if reset else 0))
+    return int(out[0])
 
 
 def spin_counters(reset: bool = False) -> tuple:

@@ -165,6 +165,10 @@ int gevo_set_nccl(int rank, int world, const void* id128) {
     return guard([&] { b200::set_nccl(rank, world, id128); });
 }
 
+int gevo_work_counters(uint64_t* out2, int reset) {
+    return guard([&] { b200::work_counters(b200::Device::default_device(), out2, reset != 0); });
+}
+
 int gevo_tp_counters(uint64_t* out2, int reset) {
     return guard([&] { b200::tp_counters(b200::Device::default_device(), out2, reset != 0); });
 }

@@ -58,6 +58,11 @@ constexpr int kStopRet = 1, kStopSync = 2, kStopTrap = 3, kStopAbort = 4, kStopI
 constexpr int kStopNone = -1; // run_unit: the thread continues
 // Fewest iterations a spin-accelerator jump may cover.
 constexpr int64_t kSpinMinJump = 4;
+// Failed spin-accelerator attempts after which a thread stops trying.
+#ifndef GEVO_SPIN_ATTEMPTS
+#define GEVO_SPIN_ATTEMPTS 20
+#endif
+constexpr uint32_t kSpinAttempts = GEVO_SPIN_ATTEMPTS;
 // ts_stop encodings (multi-phase kernels)
 constexpr uint32_t kTsFresh = 0, kTsResume = 3u << 16; // never run / resume after barrier
 constexpr uint32_t kTsRet = 1u << 16, kTsSync = 2u << 16;
@@ -252,6 +257,8 @@ struct Lane {
     // counters
     int64_t cost;
     int64_t ir;
+    uint32_t work;   // instructions this lane interpreted (diagnostic: jumps excluded,
+                     // discarded attempts included)
     int32_t poll;
     uint32_t poll2;
     uint32_t jumps;   // spin-accelerator jumps (diagnostic, saturating)
@@ -445,6 +452,7 @@ __device__ __forceinline__ void charge_block(const InterpArgs& A, Lane<kM>& L, T
     if (th.executed + n <= A.budget) {
         L.cost += from == 0 ? bcost : suffix_cost(A, L, b, from);
         L.ir += n;
+        L.work += static_cast<uint32_t>(n);
         th.executed += n;
         th.slow = false;
     } else {
@@ -461,6 +469,7 @@ __device__ __forceinline__ void refund(const InterpArgs& A, Lane<kM>& L, Thread&
     const int64_t n = static_cast<int64_t>(b.len) - from;
     L.cost -= suffix_cost(A, L, b, from);
     L.ir -= n;
+    L.work -= static_cast<uint32_t>(n);
     th.executed -= n;
 }
 
@@ -470,6 +479,7 @@ __device__ __forceinline__ bool charge_one(const InterpArgs& A, Lane<kM>& L, Thr
                                            uint32_t cls) {
     L.cost += A.cost[cls];
     ++L.ir;
+    ++L.work;
     if (++th.executed > A.budget)
         return L.trap(GEVO_BUDGET_EXCEEDED);
     return true;
@@ -498,8 +508,8 @@ __device__ __forceinline__ void spin_abandon(Spin& S, const Thread& th, Lane<kM>
 #ifndef GEVO_SPIN_BACKOFF
 #define GEVO_SPIN_BACKOFF 1 // next attempt after executed * (1 + 2^-shift): shift 1 = x1.5
 #endif
-    S.next = S.attempts > 12 ? INT64_MAX : th.executed + (th.executed >> GEVO_SPIN_BACKOFF) + 64;
-    if (S.mode == 2 && S.K < S.H && S.attempts <= 12) {
+    S.next = S.attempts > kSpinAttempts ? INT64_MAX : th.executed + (th.executed >> GEVO_SPIN_BACKOFF) + 64;
+    if (S.mode == 2 && S.K < S.H && S.attempts <= kSpinAttempts) {
         // The anchor's loop leaves its path within K + 1 iterations (an inner
         // loop running out): try again right after that, at a block other
         // than this anchor -- typically the enclosing loop, whose iterations
@@ -815,6 +825,11 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
             --S.skip;
             return;
         }
+        // after an inner loop ran out, prefer an anchor in a block laid out
+        // before it (an enclosing loop's header precedes its body) for a few
+        // of its periods, then any block but the failed anchor
+        if (S.avoid >= 0 && th.block >= S.avoid && th.executed < S.next + 4 * S.p + 256)
+            return;
         if (th.block == S.avoid)
             return;
         for (uint32_t x = 0; x < L.n_values; ++x) {
@@ -837,6 +852,43 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
             spin_abandon(S, th, L, 1);
             return;
         }
+#ifndef GEVO_SPIN_NOCHUNK
+        // (snapshot words read in chunks: independent global loads in flight
+        // together instead of one round trip per slot)
+        constexpr uint32_t kChunk = 4;
+        for (uint32_t x0 = 0; x0 < L.n_values; x0 += kChunk) {
+            uint32_t bt[kChunk], bb[kChunk];
+#pragma unroll
+            for (uint32_t k = 0; k < kChunk; ++k)
+                if (x0 + k < L.n_values) {
+                    const size_t at = sp_at(A, L, x0 + k);
+                    bt[k] = A.sp_btag[at];
+                    bb[k] = A.sp_base[at];
+                }
+#pragma unroll
+            for (uint32_t k = 0; k < kChunk; ++k) {
+                if (x0 + k >= L.n_values)
+                    break;
+                const uint2 v = L.V(x0 + k);
+                if (bt[k] != v.y) {
+                    spin_abandon(S, th, L, 2);
+                    return;
+                }
+                const size_t at = sp_at(A, L, x0 + k);
+                uint32_t d = v.x - bb[k];
+                uint8_t vary = 0;
+                if (d && !slot_strided(v.y)) {
+                    vary = 1;
+                    d = 0;
+                }
+                A.sp_delta[at] = d;
+                A.sp_base[at] = v.x;
+                A.sp_cur[at] = d;
+                A.sp_hvary[at] = vary;
+                A.sp_cvary[at] = vary;
+            }
+        }
+#else
         for (uint32_t x = 0; x < L.n_values; ++x) {
             const uint2 v = L.V(x);
             const size_t at = sp_at(A, L, x);
@@ -856,6 +908,7 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
             A.sp_hvary[at] = vary;
             A.sp_cvary[at] = vary;
         }
+#endif
         for (uint32_t x = L.n_values; x < L.n_slots; ++x) {
             A.sp_cur[sp_at(A, L, x)] = 0;
             A.sp_cvary[sp_at(A, L, x)] = 0;
@@ -1990,6 +2043,7 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
     }
     L.cost = 0;
     L.ir = 0;
+    L.work = 0;
     L.poll = 2048;
     L.jumps = 0;
     L.spin_dbg = 0;
@@ -2061,10 +2115,22 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
     rec.pad[0] = static_cast<uint8_t>(L.jumps);
     rec.pad[1] = static_cast<uint8_t>(L.spin_dbg);
     A.rec[gi] = rec;
+    if (A.counters && L.work)
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 4),
+                  static_cast<unsigned long long>(L.work));
 
     if (A.early_exit && status != GEVO_STATUS_SKIPPED &&
         (status != GEVO_STATUS_COMPLETED || error > A.tolerance))
         atomicMin(A.first_fail + v, static_cast<int32_t>(t));
+}
+
+// Interpreted-instruction counter (counters[4]): one atomic per warp.
+__device__ __forceinline__ void add_work(const InterpArgs& A, uint32_t work) {
+    unsigned long long w = work;
+    for (int o = 16; o; o >>= 1)
+        w += __shfl_xor_sync(0xffffffffu, w, o);
+    if (A.counters && (threadIdx.x & 31) == 0 && w)
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.counters + 4), w);
 }
 
 // ---- thread-parallel interpreter ---------------------------------------------
@@ -2289,6 +2355,7 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
     L.seq = false;
     L.cost = 0;
     L.ir = 0;
+    L.work = 0;
     L.poll = 16;
     L.poll2 = 0;
     L.jumps = 0;
@@ -2627,6 +2694,7 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
     if (lane_ok)
         errs[q] = worst;
     __syncthreads();
+    add_work(A, lane_ok ? L.work : 0u);
     if (A.regions && threadIdx.x == 0 && S.region != 0xFFFFFFFFu)
         region_release(A, S.region);
     if (!leader || !inst_ok)

@@ -110,8 +110,9 @@ struct InterpArgs {
     gevo_test_record* rec;          // [variant * n_tests + test]
     int32_t* first_fail;            // [variant] (early-exit mode)
     int32_t early_exit;
-    uint64_t* counters;             // [4]: accelerated spins, jumped instructions,
-                                    // tp instances re-run in id order, tp instances (nullable)
+    uint64_t* counters;             // [6]: accelerated spins, jumped instructions,
+                                    // tp instances re-run in id order, tp instances,
+                                    // interpreted instructions, reserved (nullable)
     // thread-parallel per-CTA scratch regions: a CTA takes a free region of
     // the global cells / access records / spin and snapshot columns when it
     // starts and returns it when it ends, so scratch is sized by the CTAs

@@ -418,8 +418,8 @@ int launch_all(DeviceImpl& dev, Scratch& sc, DeviceSuite& suite, gevo::InterpArg
 
     const int64_t thr = spin_threshold();
     if (!dev.counters.ptr) {
-        dev.counters.reserve(32);
-        check(cudaMemsetAsync(dev.counters.ptr, 0, 32, s), "counters");
+        dev.counters.reserve(48);
+        check(cudaMemsetAsync(dev.counters.ptr, 0, 48, s), "counters");
     }
     A.counters = dev.counters.as<uint64_t>();
     A.cta_clock = nullptr;
@@ -917,6 +917,8 @@ void read_counters(Device& devh, uint64_t out[2], bool reset, size_t first) {
 void spin_counters(Device& devh, uint64_t out[2], bool reset) { read_counters(devh, out, reset, 0); }
 
 void tp_counters(Device& devh, uint64_t out[2], bool reset) { read_counters(devh, out, reset, 2); }
+
+void work_counters(Device& devh, uint64_t out[2], bool reset) { read_counters(devh, out, reset, 4); }
 
 namespace {
 

@@ -255,7 +255,7 @@ std::vector<EvalOutcome> device_verdicts(b200::DeviceSuite& suite, const b200::E
     // search is otherwise a serial host term), joined in candidate order
     const auto t_enc = std::chrono::steady_clock::now();
     b200::BatchImage batch(suite.image());
-    constexpr size_t kPart = 64;
+    constexpr size_t kPart = 16; // (a wave holds a few hundred candidates: enough parts for every worker)
     const size_t parts = (hi - lo + kPart - 1) / kPart;
     if (jobs > 1 && parts > 1) {
         std::vector<std::unique_ptr<b200::BatchImage>> part(parts);

@@ -107,6 +107,9 @@ void spin_counters(Device& dev, uint64_t out[2], bool reset);
 // Thread-parallel interpreter counters: {instances re-run in thread-id order
 // after a same-phase cross-thread conflict, instances run}.
 void tp_counters(Device& dev, uint64_t out[2], bool reset);
+// {instructions the interpreters executed (spin-accelerator jumps excluded,
+// work of discarded attempts and aborted threads included), 0}.
+void work_counters(Device& dev, uint64_t out[2], bool reset);
 
 // Multi-GPU exchange: one process per GPU; the engine shards
 // each candidate batch across the ranks by variant and all-gathers the
