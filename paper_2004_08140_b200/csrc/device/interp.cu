@@ -1850,16 +1850,32 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
     // When every live lane is at the lead pc the warp is converged and stays
     // so until a branch: it runs units up to the next block entry before the
     // next gate (one gate per block, not per unit, on converged code).
+    // Starvation guard: the lowest live thread decides the instance's record
+    // when it stops (higher threads are then aborted), so it must not wait
+    // behind a lane spinning at lower pcs. When it has not run for 32
+    // rounds, the warp follows its pc for the next 256 rounds.
     // (An adaptive variant -- ungated until a periodic probe sees divergence
     // -- measured slower on both configs 3 and 4.)
     const bool gate = A.reconv != 0;
     unsigned live = __activemask();
+    uint32_t starve = 0, follow = 0;
     for (;;) {
         int stop = kStopNone;
         bool run = true, together = true;
         if (gate) {
-            run = pc == __reduce_min_sync(live, pc);
-            together = __all_sync(live, run);
+            const int leader = __ffs(live) - 1;
+            const uint32_t lead = follow ? __shfl_sync(live, pc, leader) : __reduce_min_sync(live, pc);
+            run = pc == lead;
+            const unsigned runs = __ballot_sync(live, run);
+            together = runs == live;
+            if (follow) {
+                --follow;
+            } else if ((runs >> leader) & 1u) {
+                starve = 0;
+            } else if (++starve >= 32) {
+                starve = 0;
+                follow = 256;
+            }
         }
         if (run) {
             bool entered = false;
