@@ -1854,15 +1854,19 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
     // when it stops (higher threads are then aborted), so it must not wait
     // behind a lane spinning at lower pcs. When it has not run for 32
     // rounds, the warp follows its pc for the next 256 rounds.
-    // (An adaptive variant -- ungated until a periodic probe sees divergence
-    // -- measured slower on both configs 3 and 4.)
+    // Yield test: when over 64 gated rounds fewer than a quarter of the live
+    // lanes ran per round, the lanes' paths do not meet (e.g. different loop
+    // trip counts, lanes that jumped a spinning loop) and waiting only
+    // serialises them: the warp runs ungated for 512 rounds, then retries.
     const bool gate = A.reconv != 0;
     unsigned live = __activemask();
-    uint32_t starve = 0, follow = 0;
+    uint32_t starve = 0, follow = 0, off = 0, rounds = 0, ran = 0;
     for (;;) {
         int stop = kStopNone;
         bool run = true, together = true;
-        if (gate) {
+        if (gate && off) {
+            --off;
+        } else if (gate) {
             const int leader = __ffs(live) - 1;
             const uint32_t lead = follow ? __shfl_sync(live, pc, leader) : __reduce_min_sync(live, pc);
             run = pc == lead;
@@ -1875,6 +1879,12 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
             } else if (++starve >= 32) {
                 starve = 0;
                 follow = 256;
+            }
+            ran += 4 * __popc(runs) >= __popc(live) ? 1u : 0u;
+            if (++rounds == 64) {
+                if (ran < 32)
+                    off = 512;
+                rounds = ran = 0;
             }
         }
         if (run) {
