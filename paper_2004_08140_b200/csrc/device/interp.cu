@@ -2296,9 +2296,9 @@ template <int kM>
 #else
 #define GEVO_TP_BOUNDS __launch_bounds__(kTpMaxBlock, 1)
 #endif
-__global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpArgs A) {
+__device__ __forceinline__ void tp_item(const InterpArgs& A, TpInst& S, uint32_t item,
+                                        uint32_t fixed_region) {
     constexpr bool kGC = kM == 3; // instance memory in global cells
-    __shared__ TpInst S;
     TpGeom G;
     G.T = static_cast<uint32_t>(A.threads);
     G.Ln = A.tp_lanes;
@@ -2313,8 +2313,8 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
     // test groups major: every variant's first tests are scheduled before any
     // later ones, so the early-exit protocol (first_fail) can skip the tests
     // the reference never runs after a failure
-    const uint32_t vl = blockIdx.x % A.n_var;
-    const uint32_t tg = blockIdx.x / A.n_var;
+    const uint32_t vl = item % A.n_var;
+    const uint32_t tg = item / A.n_var;
     const uint32_t t = tg * Ln + j;
     const uint32_t v = A.v_begin + vl;
     const bool inst_ok = t < nt;
@@ -2361,8 +2361,8 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
     L.row = 0;
     L.v = v;
     L.t = inst_ok ? t : 0;
-    L.il = blockIdx.x * 32 + j;
-    L.sl = blockIdx.x * blockDim.x + threadIdx.x;
+    L.il = item * 32 + j;
+    L.sl = item * blockDim.x + threadIdx.x;
     L.tid = static_cast<int32_t>(tid);
     L.binfo = A.buf_info + static_cast<size_t>(L.t) * A.n_params;
     L.csh = cell0 + j * 8;
@@ -2430,7 +2430,8 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
             bool any = false;
             for (uint32_t c = 0; c < Ln; ++c)
                 any |= S.state[c] != kInstDone;
-            S.region = any ? region_acquire(A) : 0xFFFFFFFFu;
+            // (a persistent CTA owns its region)
+            S.region = !any ? 0xFFFFFFFFu : fixed_region != 0xFFFFFFFFu ? fixed_region : region_acquire(A);
         }
         __syncthreads();
         const uint32_t rg = S.region;
@@ -2721,7 +2722,7 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
         errs[q] = worst;
     __syncthreads();
     add_work(A, lane_ok ? L.work : 0u);
-    if (A.regions && threadIdx.x == 0 && S.region != 0xFFFFFFFFu)
+    if (A.regions && fixed_region == 0xFFFFFFFFu && threadIdx.x == 0 && S.region != 0xFFFFFFFFu)
         region_release(A, S.region);
     if (!leader || !inst_ok)
         return;
@@ -2753,6 +2754,87 @@ __global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpAr
     if (A.early_exit && status != GEVO_STATUS_SKIPPED &&
         (status != GEVO_STATUS_COMPLETED || error > A.tolerance))
         atomicMin(A.first_fail + v, static_cast<int32_t>(t));
+}
+
+constexpr uint32_t kNoItem = 0xFFFFFFFFu;
+
+// Work item a CTA may run now: the first test group, a group whose variant
+// already failed an earlier test (a skip), or one whose earlier groups are
+// all finished.
+__device__ __forceinline__ bool tp_ready(const InterpArgs& A, uint32_t k) {
+    const uint32_t vl = k % A.n_var, tg = k / A.n_var;
+    if (tg == 0 || !A.early_exit)
+        return true;
+    const volatile int32_t* ff = A.first_fail;
+    if (ff[A.v_begin + vl] < static_cast<int32_t>(tg * A.tp_lanes))
+        return true;
+    return reinterpret_cast<const volatile uint32_t*>(A.vdone)[vl] >= tg;
+}
+
+// Persistent scheduler (thread 0 of a CTA): static test-major order, blocked
+// items deferred; then the deferred ones, ready first, else speculatively.
+__device__ uint32_t tp_next_item(const InterpArgs& A) {
+    for (;;) {
+        const uint32_t k = atomicAdd(A.sched, 1u);
+        if (k >= A.n_items)
+            break;
+        if (tp_ready(A, k))
+            return k;
+        const uint32_t slot = atomicAdd(A.sched + 1, 1u);
+        reinterpret_cast<volatile uint32_t*>(A.defer)[slot] = k;
+    }
+    const volatile uint32_t* defer = A.defer;
+    const volatile uint32_t* claim = A.claim;
+    for (;;) {
+        const uint32_t nd = reinterpret_cast<const volatile uint32_t*>(A.sched)[1];
+        int32_t spec = -1;
+        for (uint32_t e = 0; e < nd; ++e) {
+            if (claim[e])
+                continue;
+            const uint32_t k = defer[e];
+            if (k == kNoItem)
+                continue; // being written by the CTA that deferred it (it drains it)
+            if (tp_ready(A, k)) {
+                if (atomicExch(A.claim + e, 1u) == 0u)
+                    return k;
+            } else if (spec < 0) {
+                spec = static_cast<int32_t>(e);
+            }
+        }
+        if (spec < 0)
+            return kNoItem;
+        if (atomicExch(A.claim + spec, 1u) == 0u)
+            return defer[spec];
+    }
+}
+
+template <int kM>
+__global__ void GEVO_TP_BOUNDS interp_tp_kernel(const __grid_constant__ InterpArgs A) {
+    __shared__ TpInst S;
+    __shared__ uint32_t next_item;
+    for (uint32_t round = 0;; ++round) {
+        uint32_t it;
+        if (A.persist) {
+            if (threadIdx.x == 0)
+                next_item = tp_next_item(A);
+            __syncthreads();
+            it = next_item;
+            if (it == kNoItem)
+                return;
+        } else {
+            if (round)
+                return;
+            it = blockIdx.x;
+        }
+        tp_item<kM>(A, S, it, A.persist ? blockIdx.x : 0xFFFFFFFFu);
+        if (A.persist) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence(); // records and first_fail before the group counts as done
+                atomicAdd(A.vdone + it % A.n_var, 1u);
+            }
+        }
+    }
 }
 
 // Per-launch block records: {start, len | nphi << 16, cost of the block under
@@ -3016,7 +3098,9 @@ cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream) {
                                gc ? 0 : A.n_cells, gc ? 0 : A.n_chunks, A.tp_snap != nullptr, gc);
     if (s.warps_per_cta == 0 || s.lanes != A.tp_lanes)
         return cudaErrorInvalidConfiguration;
-    const unsigned grid = A.n_var * ((static_cast<uint32_t>(A.n_tests) + s.lanes - 1) / s.lanes);
+    // persistent launches: one CTA per region, items from the queue
+    const unsigned grid = A.persist ? A.regions
+                                    : A.n_var * ((static_cast<uint32_t>(A.n_tests) + s.lanes - 1) / s.lanes);
     static const int carveout = [] {
         const char* e = std::getenv("GEVO_TP_CARVEOUT"); // shared-memory carveout % (tuning)
         return e ? std::atoi(e) : -1;

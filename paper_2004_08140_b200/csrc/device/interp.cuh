@@ -121,6 +121,17 @@ struct InterpArgs {
     uint32_t* region_q;             // [regions] free-region ring: region | generation << 16
     uint32_t* region_ctr;           // [2] acquire / release tickets
     uint32_t reconv;                // run_thread reconvergence gate (lanes of one test)
+    // persistent thread-parallel launch (global cells): `regions` CTAs, CTA r
+    // owns region r and takes work items (variant, test group) from a queue
+    // in test-major order; with early exit an item whose variant's earlier
+    // test groups are still running is deferred, and runs speculatively only
+    // when nothing else is left (no speculative work while the GPU is full)
+    uint32_t persist;
+    uint32_t n_items;               // n_var * test groups
+    uint32_t* sched;                // [4]: next static item, deferred count, spare
+    uint32_t* defer;                // [n_items] deferred item ids (0xFFFFFFFF: not written yet)
+    uint32_t* claim;                // [n_items] claim flag per deferred entry
+    uint32_t* vdone;                // [n_var] finished test groups per launch-local variant
     unsigned long long* cta_clock;  // diagnostic (nullable): [variant][test] x 4 for the first
                                     // test of each thread-parallel CTA: globaltimer at CTA
                                     // start and end, SM id, device IR of the CTA

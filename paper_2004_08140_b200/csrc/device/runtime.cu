@@ -118,6 +118,7 @@ struct Scratch {
     }();
     DevBuf cta_clock; // diagnostic per-CTA timing (GEVO_CTA_CLOCK=1)
     DevBuf regions;   // thread-parallel region ring + tickets
+    DevBuf sched;     // persistent launches: queue counters, deferred items, claims, per-variant counts
 };
 
 struct DeviceImpl {
@@ -342,6 +343,17 @@ int reconv_mode() {
     return v;
 }
 
+// GEVO_TP_PERSIST=1: persistent global-cell launches with the deferring work
+// queue (measured no faster on config 4: speculative later tests only run in
+// slots the draining batch leaves idle anyway), off by default.
+bool persist_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("GEVO_TP_PERSIST");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 // GEVO_TP_REGIONS=0 gives every instance its own scratch columns (one
 // launch per scratch budget) instead of the per-CTA region pool.
 bool regions_enabled() {
@@ -470,12 +482,28 @@ int launch_all(DeviceImpl& dev, Scratch& sc, DeviceSuite& suite, gevo::InterpArg
         // launch for the whole batch (outputs read back per instance keep
         // the per-instance layout)
         A.regions = 0;
+        A.persist = 0;
         if (gc && regions_enabled() && !opt.want_outputs) {
             A.regions = gevo::tp_resident_ctas(gc, tps.warps_per_cta, tps.smem);
             chunk = std::max<uint32_t>(h.n_variants, 1);
             sc.regions.reserve((static_cast<size_t>(A.regions) + 2) * 4);
             A.region_ctr = sc.regions.as<uint32_t>();
             A.region_q = A.region_ctr + 2;
+            // persistent CTAs with the deferring work queue (GEVO_TP_PERSIST=1)
+            if (persist_enabled()) {
+                const size_t items = static_cast<size_t>(chunk) * tgroups;
+                const size_t words = 4 + 2 * items + chunk;
+                sc.sched.reserve(words * 4);
+                A.persist = 1;
+                A.n_items = static_cast<uint32_t>(items);
+                A.sched = sc.sched.as<uint32_t>();
+                A.defer = A.sched + 4;
+                A.claim = A.defer + items;
+                A.vdone = A.claim + items;
+                check(cudaMemsetAsync(A.sched, 0, 16, s), "sched");
+                check(cudaMemsetAsync(A.defer, 0xFF, items * 4, s), "sched");
+                check(cudaMemsetAsync(A.claim, 0, (items + chunk) * 4, s), "sched");
+            }
         }
         const size_t lanes = A.regions ? static_cast<size_t>(A.regions) * 32 * tps.warps_per_cta
                                        : chunk * lanes_per_variant;

@@ -59,3 +59,19 @@ for k in order:
                       "status": int(t["status"][vi, ti]), "code": int(t["code"][vi, ti]),
                       "ir": int(t["ir"][vi, ti]), "cta_ir": int(clk[vi, ti, 3]),
                       "jumps": int(t["pad"][vi, ti, 0]), "patch": cands[vi][:200]}))
+
+# occupancy timeline (CTAs running per 50 ms) and the last CTAs to finish
+ends = end[ran]
+starts = (clk[:, :, 0][ran] - t0) / 1e6
+span = float(ends.max())
+line = []
+for b in range(0, int(span) + 50, 50):
+    line.append(int(((starts < b + 50) & (ends > b)).sum()))
+print(json.dumps({"active_ctas_per_50ms": line}))
+order = np.argsort(-end, axis=None)[:10]
+for k in order:
+    vi, ti = divmod(int(k), 3)
+    if ran[vi, ti]:
+        print(json.dumps({"late_cta": [vi, ti], "start_ms": float(end[vi, ti] - dur[vi, ti]),
+                          "end_ms": float(end[vi, ti]), "status": int(t["status"][vi, ti]),
+                          "ir": int(t["ir"][vi, ti])}))

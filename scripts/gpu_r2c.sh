@@ -1,9 +1,5 @@
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_tp.py tests/test_gpu_conflicts.py tests/test_gpu_wide_conflicts.py tests/test_gpu_parity.py tests/test_gpu_spin.py tests/test_gpu_authored.py -x -q 2>&1 | tail -4
-for L in libgevo_b200.so libgevo_b200_ab.so; do
-  echo "== $L"
-  GEVO_LIB=$PWD/paper_2004_08140_b200/$L timeout 900 python scripts/diag/c4_tail.py 4096 2>&1 | cut -c1-400
-  GEVO_LIB=$PWD/paper_2004_08140_b200/$L GEVO_SCRATCH_GB=64 timeout 900 python scripts/diag/c4_tail.py 4096 2>&1 | head -1
-done
-timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['secondary']['value'], d['secondary']['ms_per_step'])"
-GEVO_LIB=$PWD/paper_2004_08140_b200/libgevo_b200_ab.so timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['secondary']['value'], d['secondary']['ms_per_step'])"
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err; python -c "import json; d=json.load(open('gpurun_out/bench.json')); print('c4', d['value'], d['ms_per_step'], 'e2e', d['e2e']['value'], 'cpu', d['cpu_baseline'], 'c2', d['secondary']['value'], d['secondary']['ms_per_step'], 'clocks', d['clocks'])"
+timeout 1800 python scripts/nsga_bench.py > gpurun_out/nsga.jsonl 2> gpurun_out/nsga.err; tail -3 gpurun_out/nsga.err; cat gpurun_out/nsga.jsonl
