@@ -188,7 +188,7 @@ typedef struct {
     uint32_t any_sync;
     uint32_t max_lits;    /* max n_lits over variants */
     uint32_t max_lane_slots; /* max n_values + max_phis over variants */
-    uint32_t pad;
+    uint32_t max_insts;   /* max instruction records of a variant (sentinels included) */
     /* byte offsets of each section from the start of the blob */
     uint64_t off_variants, off_blocks, off_insts, off_arms, off_lit_payload, off_lit_tag;
     uint64_t off_edges;

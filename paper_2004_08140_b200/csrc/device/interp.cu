@@ -164,6 +164,13 @@ __device__ __forceinline__ uint2 lds2(uint32_t a) {
 __device__ __forceinline__ void sts2(uint32_t a, uint32_t x, uint32_t y) {
     asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
 }
+__device__ __forceinline__ uint4 lds4(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(a));
+    return v;
+}
 __device__ __forceinline__ uint32_t ldsb(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
@@ -227,6 +234,8 @@ struct Lane {
     uint32_t base;   // element index of slot 0
     uint32_t row;
     // program
+    uint32_t code_sh;      // staged records (shared address of record 0), 0: global
+    uint32_t edge_sh;
     const gevo_inst* code;
     const int64_t* suffix; // per-instruction cost of the rest of its block (this launch)
     const gevo_edge* edges; // per-instruction pre-resolved branch phis
@@ -315,6 +324,18 @@ struct Lane {
             sts2(vsh + s * vstr, payload, tag);
         else
             gvf[base + s * row] = make_uint2(payload, tag);
+    }
+    // instruction / branch-edge record idx of the variant (staged copy when
+    // the CTA staged it, else the read-only global copy)
+    __device__ __forceinline__ uint4 rec(uint32_t idx) const {
+        if (kTP && code_sh)
+            return lds4(code_sh + idx * 16);
+        return __ldg(reinterpret_cast<const uint4*>(code) + idx);
+    }
+    __device__ __forceinline__ uint4 edge(uint32_t idx) const {
+        if (kTP && edge_sh)
+            return lds4(edge_sh + idx * 16);
+        return __ldg(reinterpret_cast<const uint4*>(edges) + idx);
     }
     // kTP: shared address of memory cell w of the instance
     __device__ __forceinline__ uint32_t cell(uint32_t w) const { return csh + w * cstr; }
@@ -1133,7 +1154,7 @@ __device__ __forceinline__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Th
     }
     if (n == 2 && !th.slow && !track) {
         // loop headers: both arms read before either phi writes (parallel copy)
-        const uint4 r0 = fetch_inst(L.code, b.start), r1 = fetch_inst(L.code, b.start + 1);
+        const uint4 r0 = L.rec(b.start), r1 = L.rec(b.start + 1);
         uint32_t ref0, ref1;
         uint2 v0, v1;
         if (!phi_arm(L, r0, th.prev, ref0)) {
@@ -1162,7 +1183,7 @@ __device__ __forceinline__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Th
     }
     if (n == 1) {
         // a single phi reads nothing another phi writes: no staging needed
-        const uint4 r = fetch_inst(L.code, b.start);
+        const uint4 r = L.rec(b.start);
         if (th.slow && !charge_one(A, L, th, f_cls(r)))
             return false;
         uint32_t ref;
@@ -1185,7 +1206,7 @@ __device__ __forceinline__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Th
         return true;
     }
     for (uint32_t j = 0; j < n; ++j) {
-        const uint4 r = fetch_inst(L.code, b.start + j);
+        const uint4 r = L.rec(b.start + j);
         if (th.slow && !charge_one(A, L, th, f_cls(r)))
             return false;
         uint32_t ref;
@@ -1204,7 +1225,7 @@ __device__ __forceinline__ bool enter_block(const InterpArgs& A, Lane<kM>& L, Th
         ++th.ip;
     }
     for (uint32_t j = 0; j < n; ++j) {
-        const uint4 r = fetch_inst(L.code, b.start + j);
+        const uint4 r = L.rec(b.start + j);
         const uint2 v = L.V(L.stage_base + j);
         if (!L.set(f_res(r), v.x, v.y)) {
             refund(A, L, th, b, n);
@@ -1555,7 +1576,7 @@ __device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread
     {
         // (a one-ahead prefetch across units measured slower: the loop-carried
         // copy of the prefetched record waits for the load anyway)
-        uint4 r = __ldg(code + pc);
+        uint4 r = L.rec(pc);
         uint32_t op = f_op(r);
         if (th.slow || S.mode == 2) {
             // exact per-instruction charging near the budget / abstract iterate
@@ -1579,7 +1600,7 @@ __device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread
 #ifndef GEVO_RUN_BRANCHY
                 // next record in flight while this one executes (the sentinel
                 // after every block keeps pc + 1 inside the variant)
-                const uint4 nx = __ldg(code + pc + 1);
+                const uint4 nx = L.rec(pc + 1);
 #endif
                 const uint2 x = L.V(f_a(r)), y = L.V(f_b(r));
                 const uint32_t otag = f_otag(r);
@@ -1635,7 +1656,7 @@ __device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread
 #ifndef GEVO_RUN_BRANCHY
                 r = nx;
 #else
-                r = __ldg(code + pc);
+                r = L.rec(pc);
 #endif
                 op = f_op(r);
                 if (op > GEVO_OP_FCMP || op == GEVO_OP_SDIV || op == GEVO_OP_FDIV)
@@ -1734,7 +1755,7 @@ __device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread
             th.ip = static_cast<int32_t>(pc - b.start);
 #ifndef GEVO_BR_EDGE_LATE
             // the edge record is in flight while the condition is read
-            const uint4 er = __ldg(reinterpret_cast<const uint4*>(L.edges + pc));
+            const uint4 er = L.edge(pc);
 #endif
             int32_t target = f_t0(r);
             bool second = false;
@@ -1773,7 +1794,7 @@ __device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread
                 }
             }
 #ifdef GEVO_BR_EDGE_LATE
-            const uint4 er = __ldg(reinterpret_cast<const uint4*>(L.edges + pc));
+            const uint4 er = L.edge(pc);
 #endif
             if (!enter_block(A, L, th, target, b, S,
                              second ? make_uint2(er.z, er.w) : make_uint2(er.x, er.y)))
@@ -2067,6 +2088,7 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
         L.base = il;
         L.row = A.n_inst;
     }
+    L.code_sh = L.edge_sh = 0;
     L.cost = 0;
     L.ir = 0;
     L.work = 0;
@@ -2231,6 +2253,7 @@ __global__ void region_init_kernel(uint32_t* q, uint32_t* ctr, uint32_t R) {
 }
 
 struct TpInst {
+    unsigned long long stage_bar; // mbarrier of the record staging copy
     uint32_t region;
     int32_t min_stop[32];
     uint32_t state[32];
@@ -2341,6 +2364,7 @@ __device__ __forceinline__ void tp_item(const InterpArgs& A, TpInst& S, uint32_t
     const uint32_t Q = T * Ln;
     const uint32_t pq0 = bits0 + 2 * bit_words * 4;  // kind | bar | tcode | taux (u32 x Q)
     const uint32_t err0 = (pq0 + 4 * Q * 4 + 7) & ~7u; // err (double x Q)
+    const uint32_t stage0 = (err0 + Q * 8 + 15) & ~15u;  // staged records: code | edges
     const uint32_t q = tid * Ln + j;
 
     Lane<kM> L;
@@ -2379,6 +2403,7 @@ __device__ __forceinline__ void tp_item(const InterpArgs& A, TpInst& S, uint32_t
     L.gstr = A.n_inst;
     L.epoch = 0;
     L.seq = false;
+    L.code_sh = L.edge_sh = 0;
     L.cost = 0;
     L.ir = 0;
     L.work = 0;
@@ -2447,6 +2472,28 @@ __device__ __forceinline__ void tp_item(const InterpArgs& A, TpInst& S, uint32_t
     }
 
     const gevo_variant var = A.variants[v];
+    // Stage the variant's instruction and branch-edge records in shared memory
+    // with two TMA bulk copies (one elected thread, an mbarrier counting the
+    // bytes); the interpreter then fetches every record with ld.shared.
+    uint32_t n_recs = 0;
+    if (A.stage_recs && __syncthreads_or(S.state[j] != kInstDone && active)) {
+        const uint32_t end = v + 1 < A.v_begin + A.n_var ? A.variants[v + 1].inst_base : A.n_insts_total;
+        n_recs = min(end - var.inst_base, A.stage_recs);
+        const uint32_t bar = smem_addr(&S.stage_bar);
+        if (threadIdx.x == 0) {
+            const uint32_t bytes = n_recs * 16;
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * bytes)
+                         : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(stage0), "l"(A.insts + var.inst_base), "r"(bytes), "r"(bar)
+                         : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(stage0 + A.stage_recs * 16), "l"(A.edges + var.inst_base), "r"(bytes), "r"(bar)
+                         : "memory");
+        }
+    }
     // CTA-shared tables: the variant's literals, each test's parameters
     for (uint32_t k = threadIdx.x; k < var.n_lits; k += blockDim.x)
         sts2(lit0 + k * 8, __ldg(A.lit_payload + var.lit_base + k), __ldg(A.lit_tag + var.lit_base + k));
@@ -2482,6 +2529,18 @@ __device__ __forceinline__ void tp_item(const InterpArgs& A, TpInst& S, uint32_t
         tp_init_cells(A, L, tid, T);
     }
 
+    if (n_recs) {
+        __syncthreads(); // the barrier is initialised before anyone waits on it
+        const uint32_t bar = smem_addr(&S.stage_bar);
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(done)
+                         : "r"(bar)
+                         : "memory");
+        L.code_sh = stage0;
+        L.edge_sh = stage0 + A.stage_recs * 16;
+    }
     for (;;) { // phases, CTA-uniform
         ++L.epoch;
         const uint32_t st = active ? S.state[j] : kInstDone;
@@ -3040,7 +3099,8 @@ size_t tp_smem_bytes(uint32_t threads, uint32_t lanes, const TpTables& tab, uint
     const size_t Q = static_cast<size_t>(threads) * lanes;
     const size_t vf = warps * 32 * (kTpTables ? tab.lane_slots : tab.max_slots);
     const bool compact = gc && kGcCompactVF;
-    size_t b = (compact ? (vf * 5 + 7) & ~size_t(7) : vf * 8) +
+    size_t b = static_cast<size_t>(tab.stage_recs) * 32 + 16 + // staged code + edge records
+               (compact ? (vf * 5 + 7) & ~size_t(7) : vf * 8) +
                (static_cast<size_t>(lanes) * (tab.n_params + 2) + tab.max_lits) * 8 +
                static_cast<size_t>(lanes) * n_cells * 8 * (backup ? 2 : 1) +
                2 * static_cast<size_t>(n_chunks) * warps * 32 * 4 + 4 * Q * 4;
@@ -3094,7 +3154,8 @@ cudaError_t launch_interp_tp(const InterpArgs& A, cudaStream_t stream) {
         return cudaSuccess;
     const bool gc = A.gcells != nullptr;
     const TpShape s = tp_shape(static_cast<uint32_t>(A.threads), static_cast<uint32_t>(A.n_tests),
-                               TpTables{A.lane_slots, A.max_slots, static_cast<uint32_t>(A.n_params), A.max_lits},
+                               TpTables{A.lane_slots, A.max_slots, static_cast<uint32_t>(A.n_params), A.max_lits,
+                                        A.stage_recs},
                                gc ? 0 : A.n_cells, gc ? 0 : A.n_chunks, A.tp_snap != nullptr, gc);
     if (s.warps_per_cta == 0 || s.lanes != A.tp_lanes)
         return cudaErrorInvalidConfiguration;

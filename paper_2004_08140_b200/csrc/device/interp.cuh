@@ -121,6 +121,11 @@ struct InterpArgs {
     uint32_t* region_q;             // [regions] free-region ring: region | generation << 16
     uint32_t* region_ctr;           // [2] acquire / release tickets
     uint32_t reconv;                // run_thread reconvergence gate (lanes of one test)
+    // instruction / edge records of the CTA's variant staged in shared memory
+    // by a TMA bulk copy (cp.async.bulk) at CTA start: records per CTA (the
+    // batch's max_insts), 0 = fetched from global memory (__ldg)
+    uint32_t stage_recs;
+    uint32_t n_insts_total;         // batch instruction records (variant extents)
     // persistent thread-parallel launch (global cells): `regions` CTAs, CTA r
     // owns region r and takes work items (variant, test group) from a queue
     // in test-major order; with early exit an item whose variant's earlier
@@ -180,6 +185,7 @@ struct TpTables {
     uint32_t max_slots;     // max over variants of every value-file slot
     uint32_t n_params;
     uint32_t max_lits;
+    uint32_t stage_recs;    // staged instruction + edge records per CTA (0: none)
 };
 TpShape tp_shape(uint32_t threads, uint32_t n_tests, const TpTables& tab, uint32_t n_cells,
                  uint32_t n_chunks, bool backup, bool gc = false);

@@ -343,6 +343,16 @@ int reconv_mode() {
     return v;
 }
 
+// GEVO_STAGE=0: the thread-parallel interpreter fetches instruction records
+// from global memory (__ldg) instead of a TMA-staged shared-memory copy.
+bool stage_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("GEVO_STAGE");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 // GEVO_TP_PERSIST=1: persistent global-cell launches with the deferring work
 // queue (measured no faster on config 4: speculative later tests only run in
 // slots the draining batch leaves idle anyway), off by default.
@@ -454,7 +464,10 @@ int launch_all(DeviceImpl& dev, Scratch& sc, DeviceSuite& suite, gevo::InterpArg
     const uint32_t n_chunks = std::max<uint32_t>((n_cells + 31) / 32, 1);
     const uint32_t threads = static_cast<uint32_t>(std::max(ex.threads, 1));
     // on-chip instance memory first; global cells when it does not fit
-    const gevo::TpTables tab{A.lane_slots, A.max_slots, static_cast<uint32_t>(S.n_params), A.max_lits};
+    A.stage_recs = stage_enabled() ? h.max_insts : 0;
+    A.n_insts_total = h.n_insts;
+    const gevo::TpTables tab{A.lane_slots, A.max_slots, static_cast<uint32_t>(S.n_params), A.max_lits,
+                             A.stage_recs};
     gevo::TpShape tps = gevo::tp_shape(threads, T, tab, n_cells, n_chunks, h.any_sync != 0);
     bool gc = false;
     if (tps.warps_per_cta == 0) {

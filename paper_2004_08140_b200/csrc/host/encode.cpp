@@ -6,6 +6,8 @@
 // once per variant / per suite, so the device loop only decodes integers.
 #include "encode.hpp"
 
+#include <string_view>
+
 #include <algorithm>
 #include <cstring>
 #include <map>
@@ -47,7 +49,10 @@ uint32_t buffer_word(const Buffer& b, size_t e) {
 
 bool is_global_ptr(const Param& p) { return p.type.is_ptr() && p.type.space == MemSpace::Global; }
 
-uint8_t cost_class(const Kernel& k, const Instruction& in) {
+// vtype: result type per dense value id (the last definition, as
+// operand_type's scan), empty when ids are not dense
+uint8_t cost_class(const Kernel& k, const Instruction& in,
+                   const std::vector<std::optional<Type>>& vtype) {
     switch (in.op) {
     case Opcode::Add: case Opcode::Sub: case Opcode::Mul: case Opcode::SDiv:
     case Opcode::FAdd: case Opcode::FSub: case Opcode::FMul: case Opcode::FDiv:
@@ -65,7 +70,12 @@ uint8_t cost_class(const Kernel& k, const Instruction& in) {
         // Space from the pointer operand's static type; Global when unresolved.
         bool shared = false;
         if (!in.operands.empty()) {
-            const auto t = operand_type(k, in.operands[0]);
+            const Operand& o = in.operands[0];
+            const auto t = (o.is_value() && !vtype.empty())
+                               ? (o.value >= 0 && static_cast<size_t>(o.value) < vtype.size()
+                                      ? vtype[static_cast<size_t>(o.value)]
+                                      : std::nullopt)
+                               : operand_type(k, o);
             shared = t && t->is_ptr() && t->space == MemSpace::Shared;
         }
         if (in.op == Opcode::Load)
@@ -240,6 +250,21 @@ void BatchImage::add(const Kernel& k) {
     });
     const bool dense = id_lo >= 0 && id_hi < (1 << 20);
     const size_t n_ids = dense ? static_cast<size_t>(id_hi + 1) : 0;
+    // per-kernel lookups done once: result type per value id, block index per
+    // label (Kernel::block_index scans the block list per call)
+    std::vector<std::optional<Type>> vtype(n_ids);
+    if (dense)
+        k.for_each_instruction([&](const BasicBlock&, const Instruction& in) {
+            if (in.result && *in.result >= 0)
+                vtype[static_cast<size_t>(*in.result)] = in.result_type();
+        });
+    std::unordered_map<std::string_view, int> label_ix;
+    for (size_t b = k.blocks.size(); b-- > 0;) // first block of a label wins
+        label_ix[k.blocks[b].label] = static_cast<int>(b);
+    auto bix = [&](const std::string& l) -> int {
+        const auto it = label_ix.find(l);
+        return it == label_ix.end() ? -1 : it->second;
+    };
 
     // Dense value slots in order of first appearance.
     std::unordered_map<int32_t, uint32_t> slot_map;
@@ -375,6 +400,7 @@ void BatchImage::add(const Kernel& k) {
         blocks_.push_back(gb);
         rel += gb.len + 1u; // + fell-off sentinel
     }
+    max_insts_ = std::max<uint32_t>(max_insts_, rel);
     // Branch edges: the target block's leading phis resolved for this block as
     // predecessor (first arm whose label is this block, like enter_block).
     auto edge_of = [&](int from_block, int target) -> std::pair<uint32_t, uint32_t> {
@@ -395,7 +421,7 @@ void BatchImage::add(const Kernel& k) {
             uint32_t r = GEVO_EDGE_NOINC;
             const size_t n = std::min(phi.operands.size(), phi.labels.size());
             for (size_t a = 0; a < n; ++a)
-                if (k.block_index(phi.labels[a]) == from_block) {
+                if (bix(phi.labels[a]) == from_block) {
                     r = ref(phi, a);
                     break;
                 }
@@ -411,7 +437,7 @@ void BatchImage::add(const Kernel& k) {
             if (in.op == Opcode::Br) {
                 for (size_t e = 0; e < 2; ++e) {
                     const auto pr = e < in.labels.size()
-                                        ? edge_of(this_block, k.block_index(in.labels[e]))
+                                        ? edge_of(this_block, bix(in.labels[e]))
                                         : std::pair<uint32_t, uint32_t>{GEVO_EDGE_NONE, GEVO_EDGE_NONE};
                     ge.phi[e][0] = pr.first;
                     ge.phi[e][1] = pr.second;
@@ -420,7 +446,7 @@ void BatchImage::add(const Kernel& k) {
             edges_.push_back(ge);
             gevo_inst g{};
             g.op = static_cast<uint8_t>(in.op);
-            g.cls = cost_class(k, in);
+            g.cls = cost_class(k, in, vtype);
             g.res = (in.result && *in.result >= 0) ? static_cast<uint16_t>(slot_at(*in.result))
                                                    : static_cast<uint16_t>(GEVO_NO_RESULT);
             g.t0 = g.t1 = -1;
@@ -461,16 +487,16 @@ void BatchImage::add(const Kernel& k) {
                 if (n <= 2) {
                     if (n > 0) {
                         g.a = ref(in, 0);
-                        g.t0 = static_cast<int16_t>(k.block_index(in.labels[0]));
+                        g.t0 = static_cast<int16_t>(bix(in.labels[0]));
                     }
                     if (n > 1) {
                         g.b = ref(in, 1);
-                        g.t1 = static_cast<int16_t>(k.block_index(in.labels[1]));
+                        g.t1 = static_cast<int16_t>(bix(in.labels[1]));
                     }
                 } else {
                     g.c = static_cast<uint16_t>(arms_.size() - var.arm_base);
                     for (size_t a = 0; a < n; ++a)
-                        arms_.push_back(gevo_arm{static_cast<int16_t>(k.block_index(in.labels[a])),
+                        arms_.push_back(gevo_arm{static_cast<int16_t>(bix(in.labels[a])),
                                                  ref(in, a)});
                 }
                 break;
@@ -478,9 +504,9 @@ void BatchImage::add(const Kernel& k) {
             case Opcode::Br:
                 g.aux = in.labels.size() == 2 ? 2 : 1;
                 if (!in.labels.empty())
-                    g.t0 = static_cast<int16_t>(k.block_index(in.labels[0]));
+                    g.t0 = static_cast<int16_t>(bix(in.labels[0]));
                 if (in.labels.size() == 2) {
-                    g.t1 = static_cast<int16_t>(k.block_index(in.labels[1]));
+                    g.t1 = static_cast<int16_t>(bix(in.labels[1]));
                     g.a = ref(in, 0);
                 }
                 break;
@@ -554,6 +580,7 @@ void BatchImage::append(BatchImage&& o) {
     max_values_ = std::max(max_values_, o.max_values_);
     max_lits_ = std::max(max_lits_, o.max_lits_);
     max_lane_slots_ = std::max(max_lane_slots_, o.max_lane_slots_);
+    max_insts_ = std::max(max_insts_, o.max_insts_);
     any_sync_ = any_sync_ || o.any_sync_;
     dirty_ = true;
 }
@@ -581,6 +608,7 @@ const std::vector<uint8_t>& BatchImage::blob() {
     h.any_sync = any_sync_ ? 1 : 0;
     h.max_lits = max_lits_;
     h.max_lane_slots = max_lane_slots_;
+    h.max_insts = max_insts_;
     uint64_t off = align(sizeof(gevo_batch_header));
     h.off_variants = off;
     off = align(off + variants_.size() * sizeof(gevo_variant));

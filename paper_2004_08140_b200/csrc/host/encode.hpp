@@ -89,6 +89,7 @@ private:
     uint32_t max_values_ = 0;
     uint32_t max_lits_ = 0;
     uint32_t max_lane_slots_ = 0;
+    uint32_t max_insts_ = 0;
     bool any_sync_ = false;
 };
 
