@@ -412,6 +412,10 @@ struct Thread {
     int64_t executed;
     uint32_t bar;
     bool slow; // current block runs with per-instruction charging
+    // executed count that arms the spin accelerator in the thread's next
+    // phase (-1: the launch threshold). Kept across barriers, so a thread whose
+    // loop contains a barrier does not restart an attempt every phase.
+    int64_t spin_next = -1;
 };
 
 // Current block of a thread (decoded block record).
@@ -1058,8 +1062,10 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
     S.mode = 0;
     if (n < m || S.K < m + 1) {
         // interpret past the flip, then look for the next affine stretch
-        S.attempts = 0;
+        // (re-arming only after jumps that paid for themselves measured 2x
+        // slower on config 2: its loops live on many short jumps)
         S.skip = 0;
+        S.attempts = 0;
         S.next = th.executed + 2 * S.p + 16;
     } else {
         S.next = INT64_MAX;
@@ -1780,6 +1786,13 @@ __device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread
                     L.poll = 16;
                     if (static_cast<int32_t>(lds1(L.msh)) < L.tid)
                         return kStopAbort;
+                    // global-cell instances restart from their initial state
+                    // after any same-phase conflict: stop the doomed run now
+                    // instead of running every thread to the phase end
+#ifndef GEVO_NO_CONFLICT_ABORT
+                    if (Lane<kM>::kGC && !L.seq && lds1(L.fsh))
+                        return kStopAbort;
+#endif
                     if (A.early_exit && (++L.poll2 & 127) == 0 &&
                         first_fail[L.v] < static_cast<int32_t>(L.t)) {
                         L.trap(GEVO_SKIPPED);
@@ -1857,7 +1870,7 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
     S.mode = 0;
     S.skip = 0;
     S.attempts = 0;
-    S.next = A.sp_base ? A.spin_threshold : INT64_MAX;
+    S.next = !A.sp_base ? INT64_MAX : th.spin_next >= 0 ? th.spin_next : A.spin_threshold;
     S.avoid = -1;
     S.K = S.H = 0;
     int64_t bcost;
@@ -1916,8 +1929,13 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
         }
         if (gate)
             live = __ballot_sync(live, stop == kStopNone);
-        if (stop != kStopNone)
+        if (stop != kStopNone) {
+            // a barrier ended the phase: an attempt in progress counts as a
+            // failed one (backoff) and the armed point carries over
+            if (stop == kStopSync && A.sp_base)
+                th.spin_next = S.mode != 0 ? th.executed + (th.executed >> GEVO_SPIN_BACKOFF) + 64 : S.next;
             return stop;
+        }
     }
 }
 

@@ -22,7 +22,10 @@ for a in sys.argv[1:]:
     print("==== candidate", i, cands[i])
     print(text)
     b = suite.batch().add_patch(cands[i])
+    gevo.spin_counters(reset=True)
+    gevo.work_counters(reset=True)
     _, t, st = b.eval(cfg, tolerance=0.01, early_exit=False, tests=True)
+    print(json.dumps({"spins": gevo.spin_counters(reset=True), "interpreted": gevo.work_counters(reset=True)}))
     clk = gevo.debug_cta_clock(1, 3)
     for tt in range(3):
         r = t[0, tt]

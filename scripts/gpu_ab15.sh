@@ -1,0 +1,5 @@
+timeout 1500 python -m pytest tests/test_gpu_tp.py tests/test_gpu_spin.py tests/test_gpu_fuzz.py tests/test_gpu_authored.py tests/test_gpu_wide_conflicts.py tests/test_gpu_parity.py tests/test_gpu_shapes.py -x -q 2>&1 | tail -2
+timeout 900 python scripts/diag/c4_tail.py 4096 2>&1 | grep -E "variants|active" | cut -c1-300
+timeout 300 python scripts/diag/one_c4.py 3810 2752 696 353 2>&1 | grep -E "spins|test\"\: 0|device_ms"
+timeout 600 python scripts/bench_configs.py config3 --steps 2 --cpu-seconds 0 2>&1 | tail -1 | cut -c1-100
+timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline 2>/dev/null > gpurun_out/bp.json; python -c "import json; d=json.load(open('gpurun_out/bp.json')); print('c4', d['value'], d['ms_per_step'], 'c2', d['secondary']['value'], d['secondary']['ms_per_step'])"
