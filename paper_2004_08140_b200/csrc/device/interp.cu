@@ -63,6 +63,12 @@ constexpr int64_t kSpinMinJump = 4;
 #define GEVO_SPIN_ATTEMPTS 20
 #endif
 constexpr uint32_t kSpinAttempts = GEVO_SPIN_ATTEMPTS;
+// After a partial jump: periods of the jumped loop to wait for its anchor
+// block to come round again before anchoring elsewhere.
+#ifndef GEVO_PREFER_WINDOW
+#define GEVO_PREFER_WINDOW 4
+#endif
+constexpr int64_t kPreferWindow = GEVO_PREFER_WINDOW;
 // ts_stop encodings (multi-phase kernels)
 constexpr uint32_t kTsFresh = 0, kTsResume = 3u << 16; // never run / resume after barrier
 constexpr uint32_t kTsRet = 1u << 16, kTsSync = 2u << 16;
@@ -447,7 +453,8 @@ struct Spin {
     int64_t Koob;      // iterations every strided load provably stays in bounds
     uint32_t nst, nld; // store / load log entries of the abstract iterate
     uint32_t retries;  // abstract iterates re-run with a widened hypothesis
-    int32_t avoid;     // block not to take as the next anchor (-1: none)
+    int32_t avoid;     // >= 0: block not to take as the next anchor; <= -2: block
+                       // -avoid - 2 preferred as the next anchor; -1: none
     uint32_t nvk;      // memory words whose loads are varying (sp_vk)
 };
 
@@ -857,6 +864,12 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
             return;
         if (th.block == S.avoid)
             return;
+        // after a partial jump (the loop ran to the compare flip) the next
+        // instance of the same loop is the likely spinner again (an inner
+        // loop re-entered by its enclosing loop): wait for its anchor block
+        // for a while before taking any other
+        if (S.avoid <= -2 && th.block != -S.avoid - 2 && th.executed < S.next + kPreferWindow * S.p + 64)
+            return;
         for (uint32_t x = 0; x < L.n_values; ++x) {
             const uint2 v = L.V(x);
             A.sp_base[sp_at(A, L, x)] = v.x;
@@ -1067,6 +1080,7 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
         S.skip = 0;
         S.attempts = 0;
         S.next = th.executed + 2 * S.p + 16;
+        S.avoid = -S.anchor - 2; // prefer this anchor next
     } else {
         S.next = INT64_MAX;
     }
