@@ -657,15 +657,7 @@ int launch_all(DeviceImpl& dev, Scratch& sc, DeviceSuite& suite, gevo::InterpArg
     return launches + 1;
 }
 
-uint64_t writable_union(BatchImage& batch) {
-    const auto& blob = batch.blob();
-    const auto& h = batch.header();
-    uint64_t m = 0;
-    const auto* vars = reinterpret_cast<const gevo_variant*>(blob.data() + h.off_variants);
-    for (uint32_t v = 0; v < h.n_variants; ++v)
-        m |= vars[v].writable;
-    return m;
-}
+uint64_t writable_union(BatchImage& batch) { return batch.writable_union(); }
 
 } // namespace
 
@@ -678,17 +670,17 @@ EvalResult evaluate(DeviceSuite& suite, BatchImage& batch, const ExecImage& exec
     cudaStream_t s = dev.stream;
     const SuiteImage& S = suite.image();
     EvalResult R;
-    const std::vector<uint8_t>& blob = batch.blob();
     const gevo_batch_header h = batch.header();
     const uint64_t wr = writable_union(batch);
+    const size_t bytes = h.total_bytes;
 
-    dev.h_blob.reserve(blob.size());
-    std::memcpy(dev.h_blob.ptr, blob.data(), blob.size());
-    dev.blob.reserve(blob.size() + 64); // slack: the interpreter prefetches one record ahead
+    dev.h_blob.reserve(bytes);
+    batch.write_blob(static_cast<uint8_t*>(dev.h_blob.ptr)); // straight into pinned staging
+    dev.blob.reserve(bytes + 64); // slack: the interpreter prefetches one record ahead
     check(cudaEventRecord(dev.ev0, s), "event");
-    check(cudaMemcpyAsync(dev.blob.ptr, dev.h_blob.ptr, blob.size(), cudaMemcpyHostToDevice, s),
+    check(cudaMemcpyAsync(dev.blob.ptr, dev.h_blob.ptr, bytes, cudaMemcpyHostToDevice, s),
           "blob H2D");
-    R.h2d_bytes = blob.size();
+    R.h2d_bytes = bytes;
     gevo::InterpArgs A = base_args(suite, exec, opt);
     bind_batch(A, dev.blob.ptr, h);
     check(cudaEventRecord(dev.ev1, s), "event");
@@ -748,7 +740,8 @@ EvalResult evaluate(DeviceSuite& suite, BatchImage& batch, const ExecImage& exec
     R.kernel_ms = ms;
 
     if (opt.want_outputs && total) {
-        const auto* vars = reinterpret_cast<const gevo_variant*>(blob.data() + h.off_variants);
+        const auto* vars = reinterpret_cast<const gevo_variant*>(static_cast<const uint8_t*>(dev.h_blob.ptr) +
+                                                                 h.off_variants);
         R.outputs.assign(h.n_variants, std::vector<BufferMap>(static_cast<size_t>(S.n_tests)));
         for (uint32_t v = 0; v < h.n_variants; ++v)
             for (int t = 0; t < S.n_tests; ++t) {

@@ -252,23 +252,35 @@ void BatchImage::add(const Kernel& k) {
     const size_t n_ids = dense ? static_cast<size_t>(id_hi + 1) : 0;
     // per-kernel lookups done once: result type per value id, block index per
     // label (Kernel::block_index scans the block list per call)
-    std::vector<std::optional<Type>> vtype(n_ids);
+    // per-thread working tables (capacity kept across variants)
+    struct Scratch {
+        std::vector<std::optional<Type>> vtype;
+        std::vector<int32_t> slot_flat;
+        std::vector<uint64_t> prov_flat;
+        std::vector<std::pair<uint64_t, uint32_t>> lits;
+        std::vector<int> barriers;
+    };
+    thread_local Scratch scratch;
+    std::vector<std::optional<Type>>& vtype = scratch.vtype;
+    vtype.assign(n_ids, std::nullopt);
     if (dense)
         k.for_each_instruction([&](const BasicBlock&, const Instruction& in) {
             if (in.result && *in.result >= 0)
                 vtype[static_cast<size_t>(*in.result)] = in.result_type();
         });
-    std::unordered_map<std::string_view, int> label_ix;
-    for (size_t b = k.blocks.size(); b-- > 0;) // first block of a label wins
-        label_ix[k.blocks[b].label] = static_cast<int>(b);
-    auto bix = [&](const std::string& l) -> int {
-        const auto it = label_ix.find(l);
-        return it == label_ix.end() ? -1 : it->second;
+    auto bix = [&](const std::string& l) -> int { // first block of a label wins
+        for (size_t b = 0; b < k.blocks.size(); ++b) {
+            const std::string& x = k.blocks[b].label;
+            if (x.size() == l.size() && x == l)
+                return static_cast<int>(b);
+        }
+        return -1;
     };
 
     // Dense value slots in order of first appearance.
     std::unordered_map<int32_t, uint32_t> slot_map;
-    std::vector<int32_t> slot_flat(n_ids, -1);
+    std::vector<int32_t>& slot_flat = scratch.slot_flat;
+    slot_flat.assign(n_ids, -1);
     std::vector<int32_t> slot_ids;
     auto note = [&](int32_t id) {
         if (dense) {
@@ -308,16 +320,31 @@ void BatchImage::add(const Kernel& k) {
     var.n_values = static_cast<uint16_t>(V);
     var.n_blocks = static_cast<uint16_t>(k.blocks.size());
 
+    // literal pool: a linear table while small, a hash map beyond
+    std::vector<std::pair<uint64_t, uint32_t>>& lits = scratch.lits;
+    lits.clear();
     std::unordered_map<uint64_t, uint32_t> lit_slot;
     uint32_t n_lits = 0;
     auto literal = [&](const Literal& l) -> uint16_t {
         const uint8_t tag = scalar_tag(l.kind);
         const uint32_t bits = scalar_bits(l);
         const uint64_t key = (static_cast<uint64_t>(tag) << 32) | bits;
-        const auto it = lit_slot.find(key);
-        if (it != lit_slot.end())
-            return static_cast<uint16_t>(lit_begin + it->second);
-        lit_slot.emplace(key, n_lits);
+        if (n_lits <= 32) {
+            for (const auto& [kk, sl] : lits)
+                if (kk == key)
+                    return static_cast<uint16_t>(lit_begin + sl);
+            if (n_lits == 32) // (moving to the map)
+                for (const auto& [kk, sl] : lits)
+                    lit_slot.emplace(kk, sl);
+            else
+                lits.emplace_back(key, n_lits);
+        }
+        if (n_lits >= 32) {
+            const auto it = lit_slot.find(key);
+            if (it != lit_slot.end())
+                return static_cast<uint16_t>(lit_begin + it->second);
+            lit_slot.emplace(key, n_lits);
+        }
         lit_tag_.push_back(tag);
         lit_payload_.push_back(bits);
         return static_cast<uint16_t>(lit_begin + n_lits++);
@@ -338,7 +365,8 @@ void BatchImage::add(const Kernel& k) {
     // Pointer provenance for privatising writable global buffers: pointers
     // only originate from parameters and flow through getindex and phi.
     std::unordered_map<int32_t, uint64_t> prov_map;
-    std::vector<uint64_t> prov_flat(n_ids, 0);
+    std::vector<uint64_t>& prov_flat = scratch.prov_flat;
+    prov_flat.assign(n_ids, 0);
     auto prov_ref = [&](int32_t id) -> uint64_t& {
         return dense ? prov_flat[static_cast<size_t>(id)] : prov_map[id];
     };
@@ -383,7 +411,8 @@ void BatchImage::add(const Kernel& k) {
     });
     var.writable = writable;
 
-    std::unordered_map<int, uint16_t> barrier_id;
+    std::vector<int>& barrier_uid = scratch.barriers; // barrier id = first-seen order of its uid
+    barrier_uid.clear();
     uint32_t max_phis = 0;
     uint32_t rel = 0;
     for (const BasicBlock& blk : k.blocks) {
@@ -511,8 +540,10 @@ void BatchImage::add(const Kernel& k) {
                 }
                 break;
             case Opcode::Sync: {
-                const auto it = barrier_id.emplace(in.uid, static_cast<uint16_t>(barrier_id.size()));
-                g.b = it.first->second;
+                const auto it = std::find(barrier_uid.begin(), barrier_uid.end(), in.uid);
+                g.b = static_cast<uint16_t>(it - barrier_uid.begin());
+                if (it == barrier_uid.end())
+                    barrier_uid.push_back(in.uid);
                 var.flags |= GEVO_VAR_HAS_SYNC;
                 break;
             }
@@ -586,13 +617,13 @@ void BatchImage::append(BatchImage&& o) {
 }
 
 const gevo_batch_header& BatchImage::header() {
-    blob();
+    layout();
     return hdr_;
 }
 
-const std::vector<uint8_t>& BatchImage::blob() {
+void BatchImage::layout() {
     if (!dirty_)
-        return blob_;
+        return;
     auto align = [](uint64_t x) { return (x + 15) & ~uint64_t(15); };
     gevo_batch_header h{};
     h.magic = GEVO_MAGIC;
@@ -625,12 +656,22 @@ const std::vector<uint8_t>& BatchImage::blob() {
     h.off_edges = off;
     off = align(off + edges_.size() * sizeof(gevo_edge));
     h.total_bytes = off;
-    blob_.assign(off, 0);
-    std::memcpy(blob_.data(), &h, sizeof h);
-    auto put = [&](uint64_t at, const void* src, size_t n) {
+    hdr_ = h;
+    dirty_ = false;
+    blob_.clear();
+}
+
+void BatchImage::write_blob(uint8_t* dst) {
+    layout();
+    const gevo_batch_header& h = hdr_;
+    uint64_t at = 0; // every byte written once: sections, and zeros in the alignment gaps
+    auto put = [&](uint64_t off, const void* src, size_t n) {
+        std::memset(dst + at, 0, off - at);
         if (n)
-            std::memcpy(blob_.data() + at, src, n);
+            std::memcpy(dst + off, src, n);
+        at = off + n;
     };
+    put(0, &h, sizeof h);
     put(h.off_variants, variants_.data(), variants_.size() * sizeof(gevo_variant));
     put(h.off_blocks, blocks_.data(), blocks_.size() * sizeof(gevo_block));
     put(h.off_insts, insts_.data(), insts_.size() * sizeof(gevo_inst));
@@ -638,9 +679,30 @@ const std::vector<uint8_t>& BatchImage::blob() {
     put(h.off_lit_payload, lit_payload_.data(), lit_payload_.size() * 4);
     put(h.off_lit_tag, lit_tag_.data(), lit_tag_.size());
     put(h.off_edges, edges_.data(), edges_.size() * sizeof(gevo_edge));
-    hdr_ = h;
-    dirty_ = false;
+    std::memset(dst + at, 0, h.total_bytes - at);
+}
+
+const std::vector<uint8_t>& BatchImage::blob() {
+    layout();
+    if (blob_.size() != hdr_.total_bytes) {
+        blob_.resize(hdr_.total_bytes);
+        write_blob(blob_.data());
+    }
     return blob_;
+}
+
+uint64_t BatchImage::writable_union() const {
+    uint64_t m = 0;
+    for (const gevo_variant& v : variants_)
+        m |= v.writable;
+    return m;
+}
+
+void BatchImage::reserve(size_t variants, size_t insts) {
+    variants_.reserve(variants);
+    slot_value_.reserve(variants);
+    insts_.reserve(insts);
+    edges_.reserve(insts);
 }
 
 std::string reason_text(uint8_t code, const std::string& param_name, int32_t value_id) {

@@ -64,6 +64,13 @@ public:
     // Contiguous blob in the bytecode.h layout.
     const std::vector<uint8_t>& blob();
     const gevo_batch_header& header();
+    // The same bytes written straight to `dst` (header().total_bytes of them),
+    // e.g. into a pinned staging buffer without the intermediate blob.
+    void write_blob(uint8_t* dst);
+    // Union of the variants' writable-parameter masks.
+    uint64_t writable_union() const;
+    // Capacity for `variants` variants of about `insts` records in all.
+    void reserve(size_t variants, size_t insts);
 
     // Reference reason string for a trap record of variant v.
     std::string reason(size_t v, uint8_t code, int32_t aux) const;
@@ -82,7 +89,8 @@ private:
     std::vector<uint32_t> lit_payload_;
     std::vector<uint8_t> lit_tag_;
     std::vector<std::vector<int32_t>> slot_value_; // per variant: slot -> value id
-    std::vector<uint8_t> blob_;
+    std::vector<uint8_t> blob_; // (materialised on demand by blob())
+    void layout();
     gevo_batch_header hdr_{};
     bool dirty_ = true;
     uint32_t max_slots_ = 0;

@@ -45,8 +45,13 @@ enum StreamPurpose : uint64_t {
 };
 
 // Persistent host worker pool. A search issues a few hundred parallel
-// sections (draw/apply/validate waves, encoding); spawning threads for each
-// would cost ~10^4 thread creations per run.
+// sections (draw/apply/validate waves, encoding) about a millisecond apart;
+// spawning threads for each would cost ~10^4 thread creations per run, and a
+// condition-variable wake per section costs tens of microseconds. Workers
+// spin on a section word for a while before they sleep, and claim seats in
+// it with one CAS: [epoch:32][pending:16][seats:16] -- seats still open in
+// this section, helpers inside it. The caller revokes unclaimed seats once
+// every index is taken and waits only for helpers already inside.
 class HostPool {
 public:
     static HostPool& get() {
@@ -57,31 +62,34 @@ public:
     // first exception is rethrown after every participant stopped.
     void run(size_t n, int jobs, const std::function<void(size_t)>& fn) {
         std::unique_lock<std::mutex> section(section_mu_); // one section at a time
-        Job job;
-        job.fn = &fn;
-        job.n = n;
-        const int helpers = static_cast<int>(std::min<size_t>(
-            {static_cast<size_t>(std::max(jobs - 1, 0)), workers_.size(), n - 1}));
-        {
+        const uint64_t helpers = std::min<size_t>(
+            {static_cast<size_t>(std::max(jobs - 1, 0)), workers_.size(), n - 1, 0xFFFF});
+        fn_ = &fn;
+        n_ = n;
+        next_.store(0);
+        stop_.store(false);
+        err_ = nullptr;
+        const uint64_t e = ++epoch_ & 0xFFFFFFFFu;
+        word_.store((e << 32) | helpers); // publish the section
+        if (sleepers_.load() > 0) {
             std::lock_guard<std::mutex> g(mu_);
-            job_ = &job;
-            job.pending = helpers;
-            job.seats = helpers;
-            ++gen_;
+            cv_.notify_all();
         }
-        cv_.notify_all();
-        work(job);
-        std::unique_lock<std::mutex> g(mu_);
-        done_cv_.wait(g, [&] { return job.pending == 0; });
-        job_ = nullptr;
-        g.unlock();
-        if (job.err)
-            std::rethrow_exception(job.err);
+        work();
+        // revoke the seats nobody took, then wait for the helpers inside
+        uint64_t w = word_.load();
+        while ((w & 0xFFFF) && !word_.compare_exchange_weak(w, w & ~uint64_t(0xFFFF))) {
+        }
+        for (int spin = 0; ((word_.load() >> 16) & 0xFFFF) != 0; ++spin)
+            if (spin > 1000)
+                std::this_thread::yield();
+        if (err_)
+            std::rethrow_exception(err_);
     }
     ~HostPool() {
         {
             std::lock_guard<std::mutex> g(mu_);
-            quit_ = true;
+            quit_.store(true);
         }
         cv_.notify_all();
         for (auto& t : workers_)
@@ -92,16 +100,7 @@ public:
     bool usable() const { return ::getpid() == pid_; }
 
 private:
-    struct Job {
-        const std::function<void(size_t)>* fn = nullptr;
-        size_t n = 0;
-        std::atomic<size_t> next{0};
-        std::atomic<bool> stop{false};
-        int pending = 0; // helpers still to finish (under mu_)
-        int seats = 0;   // helpers still to join (under mu_)
-        std::exception_ptr err;
-        std::mutex err_mu;
-    };
+    static constexpr int kSpin = 1 << 16; // ~1 ms of pause loops before sleeping
     static bool& worker_flag() {
         static thread_local bool f = false;
         return f;
@@ -111,48 +110,66 @@ private:
         for (unsigned w = 0; w + 1 < hw; ++w)
             workers_.emplace_back([this] { loop(); });
     }
-    static void work(Job& job) {
+    void work() {
         for (;;) {
-            const size_t i = job.next.fetch_add(1);
-            if (i >= job.n || job.stop.load())
+            const size_t i = next_.fetch_add(1);
+            if (i >= n_ || stop_.load())
                 return;
             try {
-                (*job.fn)(i);
+                (*fn_)(i);
             } catch (...) {
-                std::lock_guard<std::mutex> g(job.err_mu);
-                if (!job.err)
-                    job.err = std::current_exception();
-                job.stop.store(true);
+                std::lock_guard<std::mutex> g(err_mu_);
+                if (!err_)
+                    err_ = std::current_exception();
+                stop_.store(true);
                 return;
             }
         }
+    }
+    static bool open(uint64_t w, uint64_t seen) { return (w >> 32) != seen && (w & 0xFFFF) != 0; }
+    static void relax() {
+#if defined(__x86_64__)
+        __builtin_ia32_pause();
+#endif
     }
     void loop() {
         worker_flag() = true;
         uint64_t seen = 0;
         for (;;) {
-            Job* job = nullptr;
-            {
-                std::unique_lock<std::mutex> g(mu_);
-                cv_.wait(g, [&] { return quit_ || (gen_ != seen && job_ && job_->seats > 0); });
-                if (quit_)
+            uint64_t w = word_.load();
+            for (int spin = 0; !open(w, seen); w = word_.load()) {
+                if (quit_.load())
                     return;
-                seen = gen_;
-                job = job_;
-                --job->seats;
+                if (++spin < kSpin) {
+                    relax();
+                    continue;
+                }
+                std::unique_lock<std::mutex> g(mu_);
+                sleepers_.fetch_add(1);
+                cv_.wait(g, [&] { return quit_.load() || open(word_.load(), seen); });
+                sleepers_.fetch_sub(1);
+                spin = 0;
             }
-            work(*job);
-            std::lock_guard<std::mutex> g(mu_);
-            if (--job->pending == 0)
-                done_cv_.notify_all();
+            // claim a seat: seats - 1, pending + 1 (fails if the section moved on)
+            if (!word_.compare_exchange_weak(w, w - 1 + (uint64_t(1) << 16)))
+                continue;
+            seen = w >> 32;
+            work();
+            word_.fetch_sub(uint64_t(1) << 16);
         }
     }
     std::vector<std::thread> workers_;
-    std::mutex section_mu_, mu_;
-    std::condition_variable cv_, done_cv_;
-    Job* job_ = nullptr;
-    uint64_t gen_ = 0;
-    bool quit_ = false;
+    std::mutex section_mu_, mu_, err_mu_;
+    std::condition_variable cv_;
+    std::atomic<uint64_t> word_{0};
+    std::atomic<int> sleepers_{0};
+    std::atomic<bool> quit_{false};
+    uint64_t epoch_ = 0;
+    const std::function<void(size_t)>* fn_ = nullptr;
+    size_t n_ = 0;
+    std::atomic<size_t> next_{0};
+    std::atomic<bool> stop_{false};
+    std::exception_ptr err_;
     pid_t pid_;
 };
 
@@ -259,18 +276,21 @@ std::vector<EvalOutcome> device_verdicts(b200::DeviceSuite& suite, const b200::E
     const size_t parts = (hi - lo + kPart - 1) / kPart;
     if (jobs > 1 && parts > 1) {
         std::vector<std::unique_ptr<b200::BatchImage>> part(parts);
+        const size_t rec_hint = (ks[lo]->instruction_count() + ks[lo]->blocks.size()) * kPart * 5 / 4;
         host_parallel(parts, jobs, [&](size_t p) {
             part[p] = std::make_unique<b200::BatchImage>(suite.image());
+            part[p]->reserve(kPart, rec_hint);
             for (size_t v = lo + p * kPart; v < std::min(hi, lo + (p + 1) * kPart); ++v)
                 part[p]->add(*ks[v]);
         });
+        batch.reserve(hi - lo, rec_hint * parts);
         for (auto& p : part)
             batch.append(std::move(*p));
     } else {
         for (size_t v = lo; v < hi; ++v)
             batch.add(*ks[v]);
     }
-    batch.blob(); // serialise here, so the encode time below covers it
+    batch.header(); // lay out here, so the encode time below covers it
     ctr.host_gen_ms += ms_since(t_enc);
     b200::EvalOptions opt;
     opt.tolerance = tol;
@@ -704,14 +724,14 @@ void Engine::step_generation() {
     Rng trng = Rng::stream(cfg_.master_seed, gen, 0, kStreamTournament);
     const std::vector<int> off_idx = tournament_select(rank_, population_.size(), pop, trng);
     const std::vector<int> elite_idx = select_best(rank_, pop / 4);
-    std::vector<Individual> offspring;
-    offspring.reserve(pop);
-    for (int i : off_idx)
-        offspring.push_back(population_[static_cast<size_t>(i)]);
-    std::vector<Individual> elites;
-    elites.reserve(elite_idx.size());
-    for (int i : elite_idx)
-        elites.push_back(population_[static_cast<size_t>(i)]);
+    // (copies of selected individuals: one kernel copy each, on the pool)
+    std::vector<Individual> offspring(off_idx.size()), elites(elite_idx.size());
+    host_parallel(off_idx.size() + elite_idx.size(), cfg_.jobs, [&](size_t i) {
+        if (i < off_idx.size())
+            offspring[i] = population_[static_cast<size_t>(off_idx[i])];
+        else
+            elites[i - off_idx.size()] = population_[static_cast<size_t>(elite_idx[i - off_idx.size()])];
+    });
 
     Rng gx = Rng::stream(cfg_.master_seed, gen, 0, kStreamGateCross);
     Rng gm = Rng::stream(cfg_.master_seed, gen, 0, kStreamGateMutate);

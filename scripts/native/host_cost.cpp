@@ -49,6 +49,8 @@ int main(int argc, char** argv) {
     }
     const int per = 24;
     double t_ctx = 0, t_mut = 0, t_apply = 0, t_valid = 0, t_cx = 0, t_cxvalid = 0;
+    double t_kind[kOperatorCount] = {};
+    size_t n_kind[kOperatorCount] = {};
     size_t n_mut = 0, n_apply = 0, n_cx = 0;
     std::vector<Kernel> cands;
     Rng rng(11);
@@ -66,6 +68,8 @@ int main(int argc, char** argv) {
             ++n_mut;
             if (!m)
                 continue;
+            t_kind[static_cast<size_t>(operator_kind(*m))] += us(u0, u1);
+            ++n_kind[static_cast<size_t>(operator_kind(*m))];
             ApplyResult ap = apply_edit(parents[i], *m);
             auto u2 = Clock::now();
             t_apply += us(u1, u2);
@@ -103,9 +107,13 @@ int main(int argc, char** argv) {
     std::printf("{\"bench\": \"%s\", \"parents\": %zu, \"ctx_us_per_parent\": %.2f, "
                 "\"mutation_us\": %.2f, \"apply_edit_us\": %.2f, \"validate_us\": %.2f, "
                 "\"cx_apply_patch_us_per_child\": %.2f, \"cx_validate_us_per_child\": %.2f, "
-                "\"encode_us_per_variant\": %.2f, \"candidates\": %zu}\n",
+                "\"encode_us_per_variant\": %.2f, \"candidates\": %zu, \"mutation_us_by_kind\": {",
                 name.c_str(), parents.size(), t_ctx / parents.size(), t_mut / n_mut,
                 t_apply / n_mut, t_valid / std::max<size_t>(n_apply, 1), t_cx / n_cx,
                 t_cxvalid / n_cx, t_enc / std::max<size_t>(cands.size(), 1), cands.size());
+    for (size_t o = 0; o < kOperatorCount; ++o)
+        std::printf("%s\"%s\": %.2f", o ? ", " : "", operator_kind_name(static_cast<OperatorKind>(o)),
+                    t_kind[o] / std::max<size_t>(n_kind[o], 1));
+    std::printf("}}\n");
     return 0;
 }
