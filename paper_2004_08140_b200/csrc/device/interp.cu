@@ -1076,10 +1076,18 @@ __device__ __forceinline__ void spin_at_entry(const InterpArgs& A, Lane<kM>& L, 
     if (n < m || S.K < m + 1) {
         // interpret past the flip, then look for the next affine stretch
         // (re-arming only after jumps that paid for themselves measured 2x
-        // slower on config 2: its loops live on many short jumps)
-        S.skip = 0;
-        S.attempts = 0;
-        S.next = th.executed + 2 * S.p + 16;
+        // slower on config 2: its loops live on many short jumps); a jump
+        // short against the value file the attempt walks backs off instead
+        if (n * S.p < static_cast<int64_t>(A.spin_pay) * L.n_values) {
+            ++S.attempts;
+            S.skip = S.attempts & 3u;
+            S.next = S.attempts > kSpinAttempts ? INT64_MAX
+                                                : th.executed + (th.executed >> GEVO_SPIN_BACKOFF) + 64;
+        } else {
+            S.skip = 0;
+            S.attempts = 0;
+            S.next = th.executed + 2 * S.p + 16;
+        }
         S.avoid = -S.anchor - 2; // prefer this anchor next
     } else {
         S.next = INT64_MAX;

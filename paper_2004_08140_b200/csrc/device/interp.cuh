@@ -90,6 +90,8 @@ struct InterpArgs {
     uint32_t* sp_ld;                // [kSpinLog][inst] load-log keys
     uint32_t* sp_vk;                // [kSpinLog][col] memory words loaded as varying
     int64_t spin_threshold;         // per-thread executed count that arms it
+    uint32_t spin_pay;              // a partial jump must skip >= spin_pay * n_values
+                                    // instructions to re-arm at once (else: backoff)
     uint32_t n_spin;                // spin scratch columns (instances, or lanes for tp)
 
     // thread-parallel lanes (interp_tp_kernel)

@@ -623,18 +623,19 @@ cudaError_t rank_reserve(RankWorkspace& w, int32_t n) {
     if (e != cudaSuccess)
         return e;
     char* p = static_cast<char*>(w.mem);
+    // inputs, then every output in one span (one copy each way, see rank_impl)
     w.cost = carve<double>(p, N);
     w.err = carve<double>(p, N);
     w.crowd = carve<double>(p, N);
-    w.kc = carve<uint64_t>(p, N);
-    w.ke = carve<uint64_t>(p, N);
-    w.k0 = carve<uint64_t>(p, N);
-    w.k1 = carve<uint64_t>(p, N);
     w.front = carve<int32_t>(p, N);
     w.members = carve<int32_t>(p, N);
     w.offsets = carve<int32_t>(p, N + 1);
     w.select = carve<int32_t>(p, N);
     w.meta = carve<int32_t>(p, kMetaCount);
+    w.kc = carve<uint64_t>(p, N);
+    w.ke = carve<uint64_t>(p, N);
+    w.k0 = carve<uint64_t>(p, N);
+    w.k1 = carve<uint64_t>(p, N);
     w.seg = carve<int32_t>(p, 4);
     w.A = carve<int32_t>(p, N);
     w.B = carve<int32_t>(p, N);

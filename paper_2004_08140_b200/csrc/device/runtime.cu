@@ -128,6 +128,7 @@ struct DeviceImpl {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     DevBuf blob, counters, rank;
     gevo::RankWorkspace rws; // GPU rank_population / select_best buffers
+    PinnedBuf h_rank;        // their host staging (inputs in, outputs back)
     ncclComm_t nccl = nullptr; // record exchange of a multi-GPU search
     int nccl_rank = 0, nccl_world = 0;
     DevBuf gathered;           // all-gathered variant records
@@ -302,6 +303,18 @@ int64_t spin_threshold() {
     static const int64_t v = [] {
         const char* e = std::getenv("GEVO_SPIN_THRESHOLD");
         return e ? std::atoll(e) : int64_t(256);
+    }();
+    return v;
+}
+
+// Spin accelerator pay factor (GEVO_SPIN_PAY): an attempt costs the lane a
+// few passes over its value file in global scratch, so a partial jump that
+// skipped fewer than spin_pay * n_values instructions backs off like a failed
+// attempt instead of re-arming at once (0: always re-arm).
+uint32_t spin_pay() {
+    static const uint32_t v = [] {
+        const char* e = std::getenv("GEVO_SPIN_PAY");
+        return e ? static_cast<uint32_t>(std::atoi(e)) : 256u;
     }();
     return v;
 }
@@ -527,6 +540,7 @@ int launch_all(DeviceImpl& dev, Scratch& sc, DeviceSuite& suite, gevo::InterpArg
         if (thr > 0) {
             reserve_spin(sc, A, lanes);
             A.spin_threshold = thr;
+            A.spin_pay = spin_pay();
         }
         A.tp_snap = nullptr;
         A.out_cells = nullptr;
@@ -620,6 +634,7 @@ int launch_all(DeviceImpl& dev, Scratch& sc, DeviceSuite& suite, gevo::InterpArg
     if (thr > 0) {
         reserve_spin(sc, A, cap);
         A.spin_threshold = thr;
+        A.spin_pay = spin_pay();
     }
     if (opt.want_outputs && ow) {
         if (chunk < h.n_variants)
@@ -981,46 +996,47 @@ int32_t rank_impl(Device& devh, const std::vector<FitnessVector>& fits, bool sin
     gevo::RankWorkspace& w = dev.rws;
     check(gevo::rank_reserve(w, n), "rank buffers");
     const size_t N = static_cast<size_t>(n);
-    std::vector<double> hc(N), he(N);
+    // one pinned H2D of the input span (cost, err) and one D2H of the output
+    // span (crowd .. meta; select .. meta when only the selection is wanted),
+    // laid out as the workspace carves them
+    auto* base = reinterpret_cast<char*>(w.cost);
+    const size_t err_at = reinterpret_cast<char*>(w.err) - base;
+    const size_t in_bytes = err_at + N * 8;
+    char* out0 = reinterpret_cast<char*>(r ? static_cast<void*>(w.crowd) : static_cast<void*>(w.select));
+    const size_t out_bytes = reinterpret_cast<char*>(w.meta + gevo::kMetaCount) - out0;
+    dev.h_rank.reserve(std::max(in_bytes, out_bytes));
+    char* h = static_cast<char*>(dev.h_rank.ptr);
+    auto* hc = reinterpret_cast<double*>(h);
+    auto* he = reinterpret_cast<double*>(h + err_at);
     for (size_t i = 0; i < N; ++i) {
         hc[i] = fits[i].cost;
         he[i] = fits[i].error;
     }
-    check(cudaMemcpyAsync(w.cost, hc.data(), N * 8, cudaMemcpyHostToDevice, s), "rank H2D");
-    check(cudaMemcpyAsync(w.err, he.data(), N * 8, cudaMemcpyHostToDevice, s), "rank H2D");
+    check(cudaMemcpyAsync(base, h, in_bytes, cudaMemcpyHostToDevice, s), "rank H2D");
     check(cudaEventRecord(dev.ev0, s), "event");
     check(gevo::launch_rank(w, n, single_group, static_cast<int32_t>(keep), s), "rank kernels");
     check(cudaEventRecord(dev.ev1, s), "event");
-    int32_t meta[gevo::kMetaCount] = {};
-    std::vector<int32_t> front, members, offsets;
-    if (r) {
-        front.resize(N);
-        members.resize(N);
-        offsets.resize(N + 1);
-        check(cudaMemcpyAsync(front.data(), w.front, N * 4, cudaMemcpyDeviceToHost, s), "rank D2H");
-        check(cudaMemcpyAsync(members.data(), w.members, N * 4, cudaMemcpyDeviceToHost, s), "rank D2H");
-        check(cudaMemcpyAsync(offsets.data(), w.offsets, (N + 1) * 4, cudaMemcpyDeviceToHost, s),
-              "rank D2H");
-        check(cudaMemcpyAsync(r->crowding.data(), w.crowd, N * 8, cudaMemcpyDeviceToHost, s), "rank D2H");
-    }
-    if (best && keep > 0) {
-        best->resize(static_cast<size_t>(keep));
-        check(cudaMemcpyAsync(best->data(), w.select, static_cast<size_t>(keep) * 4,
-                              cudaMemcpyDeviceToHost, s),
-              "select D2H");
-    }
-    check(cudaMemcpyAsync(meta, w.meta, sizeof(meta), cudaMemcpyDeviceToHost, s), "rank D2H");
+    check(cudaMemcpyAsync(h, out0, out_bytes, cudaMemcpyDeviceToHost, s), "rank D2H"); // (after the H2D)
     check(cudaStreamSynchronize(s), "rank");
     if (device_ms)
         check(cudaEventElapsedTime(device_ms, dev.ev0, dev.ev1), "elapsed");
+    auto at = [&](const void* dptr) { return h + (reinterpret_cast<const char*>(dptr) - out0); };
+    const auto* meta = reinterpret_cast<const int32_t*>(at(w.meta));
     const int32_t F = meta[gevo::kMetaFronts];
+    if (best && keep > 0) {
+        const auto* sel = reinterpret_cast<const int32_t*>(at(w.select));
+        best->assign(sel, sel + keep);
+    }
     if (r) {
-        for (size_t i = 0; i < N; ++i)
-            r->front[i] = front[i];
+        const auto* cr = reinterpret_cast<const double*>(at(w.crowd));
+        const auto* front = reinterpret_cast<const int32_t*>(at(w.front));
+        const auto* members = reinterpret_cast<const int32_t*>(at(w.members));
+        const auto* offsets = reinterpret_cast<const int32_t*>(at(w.offsets));
+        r->crowding.assign(cr, cr + N);
+        r->front.assign(front, front + N);
         r->fronts.resize(static_cast<size_t>(F));
         for (int32_t f = 0; f < F; ++f)
-            r->fronts[static_cast<size_t>(f)].assign(members.begin() + offsets[static_cast<size_t>(f)],
-                                                     members.begin() + offsets[static_cast<size_t>(f) + 1]);
+            r->fronts[static_cast<size_t>(f)].assign(members + offsets[f], members + offsets[f + 1]);
     }
     return F;
 }

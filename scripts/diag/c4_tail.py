@@ -1,4 +1,4 @@
-"""GPU probe: what sets the config-4 step time. Evaluates the bench's
+"""GPU probe: what sets the config-4 step time (c4_tail.py [n [seed]]). Evaluates the bench's
 config-4 batch with per-test records and per-CTA timing (GEVO_CTA_CLOCK=1),
 then prints: the step makespan, SM-time by the class of the variant's first
 test (completed / trap / budget) and of the CTA's role (the test the reference
@@ -16,7 +16,8 @@ sys.path.insert(0, ROOT)
 import paper_2004_08140_b200 as gevo  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
-with gzip.open(os.path.join(ROOT, "bench_data", "cand_conv-bn_s1.txt.gz"), "rt") as f:
+seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1  # committed candidate set
+with gzip.open(os.path.join(ROOT, "bench_data", "cand_conv-bn_s%d.txt.gz" % seed), "rt") as f:
     cands = [x for x in f.read().splitlines() if x.strip()][:n]
 ir, gen = gevo.authored_kernel("conv-bn")
 suite = gevo.Suite.from_spec(ir, gen, 3, gevo.train_seed(1))

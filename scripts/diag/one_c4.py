@@ -1,5 +1,5 @@
 """GPU probe: one config-4 candidate alone (batch of one), its IR, records and
-CTA times, gate on and off. Usage: one_c4.py <candidate index> [...]"""
+CTA times. Usage: [C4_SEED=s] one_c4.py <candidate index> [...]"""
 import gzip
 import json
 import os
@@ -11,7 +11,8 @@ sys.path.insert(0, ROOT)
 os.environ.setdefault("GEVO_CTA_CLOCK", "1")
 import paper_2004_08140_b200 as gevo  # noqa: E402
 
-with gzip.open(os.path.join(ROOT, "bench_data", "cand_conv-bn_s1.txt.gz"), "rt") as f:
+SEED = int(os.environ.get("C4_SEED", "1"))  # committed candidate set
+with gzip.open(os.path.join(ROOT, "bench_data", "cand_conv-bn_s%d.txt.gz" % SEED), "rt") as f:
     cands = [x for x in f.read().splitlines() if x.strip()]
 ir, gen = gevo.authored_kernel("conv-bn")
 suite = gevo.Suite.from_spec(ir, gen, 3, gevo.train_seed(1))

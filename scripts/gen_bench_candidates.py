@@ -6,8 +6,10 @@ reference arm reads the same candidates without loading the product library.
 
 config 4: conv-bn (authored CIFAR-shaped conv3x3+bias+batch-norm), 4096
 mutants of up to 3 edits, seed 1. config 2: hot-branch / nw-sync / bfs-load,
-1024 mutants of up to 4 edits each, seed 1. Ranks > 0 of a multi-GPU bench
-draw their own batches with seed 1 + rank at run time."""
+1024 mutants of up to 4 edits each, seed 1; rank r of a multi-GPU bench reads
+seed 1 + r (seeds 1-8 are committed: one node of 8 GPUs).
+
+  python scripts/gen_bench_candidates.py [seeds, default 1-8]"""
 import gzip
 import os
 import sys
@@ -28,12 +30,18 @@ def candidates(kind, seed):
 
 def main():
     os.makedirs(OUT, exist_ok=True)
-    for k in ("conv-bn", "hot-branch", "nw-sync", "bfs-load"):
-        lines = candidates(k, 1)
-        path = os.path.join(OUT, "cand_%s_s1.txt.gz" % k)
-        with gzip.open(path, "wt", compresslevel=9) as f:
-            f.write("\n".join(lines) + "\n")
-        print(path, len(lines))
+    seeds = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else range(1, 9)
+    for seed in seeds:
+        for k in ("conv-bn", "hot-branch", "nw-sync", "bfs-load"):
+            write(k, seed)
+
+
+def write(k, seed):
+    lines = candidates(k, seed)
+    path = os.path.join(OUT, "cand_%s_s%d.txt.gz" % (k, seed))
+    with gzip.GzipFile(path, "wb", compresslevel=9, mtime=0) as f:  # (reproducible bytes)
+        f.write(("\n".join(lines) + "\n").encode())
+    print(path, len(lines))
 
 
 if __name__ == "__main__":

@@ -5,13 +5,14 @@
 //
 //   g++ -std=c++20 -O2 -Iinclude -Ipaper_2004_08140_b200/csrc -I$JSON_DIR \
 //       scripts/native/host_cost.cpp paper_2004_08140_b200/libgevo_b200.so -o /tmp/host_cost
-//   /tmp/host_cost nw-sync
+//   /tmp/host_cost nw-sync [max walk depth, default 6]
 #include "evoir/corpus.hpp"
 #include "evoir/operators.hpp"
 #include "host/encode.hpp"
 
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 
 using namespace evoir;
 using Clock = std::chrono::steady_clock;
@@ -22,6 +23,7 @@ static double us(Clock::time_point a, Clock::time_point b) {
 
 int main(int argc, char** argv) {
     const std::string name = argc > 1 ? argv[1] : "nw-sync";
+    const int max_depth = argc > 2 ? std::max(1, std::atoi(argv[2])) : 6;
     const Benchmark bm = load_benchmark(name);
     const Kernel& orig = bm.kernel;
     // parents: accepted-by-validate random walks of up to 6 edits
@@ -31,7 +33,7 @@ int main(int argc, char** argv) {
     while (parents.size() < 256) {
         Kernel k = orig;
         Patch p;
-        const int depth = 1 + static_cast<int>(walk.index(6));
+        const int depth = 1 + static_cast<int>(walk.index(static_cast<size_t>(max_depth)));
         for (int d = 0; d < depth; ++d) {
             const DomTree dom = DomTree::build(k);
             MutationContext ctx(k, dom, walk);
