@@ -46,6 +46,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 namespace gevo {
@@ -220,8 +221,16 @@ constexpr bool kGcCompactVF = true;
 constexpr bool kGcCompactVF = false;
 #endif
 
+// Record pointers of the global-cell lanes (empty for the other modes, so
+// their lanes carry no unused fields).
+struct LaneRecs {
+    const uint4* rp;       // generic pointer to record 0 (the TMA-staged copy in shared
+    const uint4* ep;       // memory, or global memory): one load instruction either way
+};
+struct LaneNoRecs {};
+
 template <int kM>
-struct Lane {
+struct Lane : std::conditional_t<kM == 3, LaneRecs, LaneNoRecs> {
     static constexpr bool kSmem = kM >= 1;
     static constexpr bool kTP = kM >= 2;
     static constexpr bool kGC = kM == 3; // instance memory cells in global memory
@@ -240,8 +249,6 @@ struct Lane {
     uint32_t base;   // element index of slot 0
     uint32_t row;
     // program
-    uint32_t code_sh;      // staged records (shared address of record 0), 0: global
-    uint32_t edge_sh;
     const gevo_inst* code;
     const int64_t* suffix; // per-instruction cost of the rest of its block (this launch)
     const gevo_edge* edges; // per-instruction pre-resolved branch phis
@@ -331,16 +338,17 @@ struct Lane {
         else
             gvf[base + s * row] = make_uint2(payload, tag);
     }
-    // instruction / branch-edge record idx of the variant (staged copy when
-    // the CTA staged it, else the read-only global copy)
+    // instruction / branch-edge record idx of the variant (global-cell
+    // kernels: the staged copy when the CTA staged it, through a generic
+    // pointer; else the read-only global copy)
     __device__ __forceinline__ uint4 rec(uint32_t idx) const {
-        if (kTP && code_sh)
-            return lds4(code_sh + idx * 16);
+        if constexpr (kGC)
+            return this->rp[idx];
         return __ldg(reinterpret_cast<const uint4*>(code) + idx);
     }
     __device__ __forceinline__ uint4 edge(uint32_t idx) const {
-        if (kTP && edge_sh)
-            return lds4(edge_sh + idx * 16);
+        if constexpr (kGC)
+            return this->ep[idx];
         return __ldg(reinterpret_cast<const uint4*>(edges) + idx);
     }
     // kTP: shared address of memory cell w of the instance
@@ -2128,7 +2136,6 @@ __global__ void __launch_bounds__(128) interp_kernel(const __grid_constant__ Int
         L.base = il;
         L.row = A.n_inst;
     }
-    L.code_sh = L.edge_sh = 0;
     L.cost = 0;
     L.ir = 0;
     L.work = 0;
@@ -2443,7 +2450,6 @@ __device__ __forceinline__ void tp_item(const InterpArgs& A, TpInst& S, uint32_t
     L.gstr = A.n_inst;
     L.epoch = 0;
     L.seq = false;
-    L.code_sh = L.edge_sh = 0;
     L.cost = 0;
     L.ir = 0;
     L.work = 0;
@@ -2546,6 +2552,10 @@ __device__ __forceinline__ void tp_item(const InterpArgs& A, TpInst& S, uint32_t
         L.code = A.insts + var.inst_base;
         L.suffix = A.suffix ? A.suffix + var.inst_base : nullptr;
         L.edges = A.edges + var.inst_base;
+        if constexpr (Lane<kM>::kGC) {
+            L.rp = reinterpret_cast<const uint4*>(L.code);
+            L.ep = reinterpret_cast<const uint4*>(L.edges);
+        }
         L.dblk = A.dblocks + var.block_base;
         L.arm = A.arms + var.arm_base;
         L.n_values = var.n_values;
@@ -2578,8 +2588,11 @@ __device__ __forceinline__ void tp_item(const InterpArgs& A, TpInst& S, uint32_t
                          : "=r"(done)
                          : "r"(bar)
                          : "memory");
-        L.code_sh = stage0;
-        L.edge_sh = stage0 + A.stage_recs * 16;
+        if constexpr (Lane<kM>::kGC) {
+            const char* g0 = reinterpret_cast<const char*>(g_vfs) + (stage0 - sbase); // generic
+            L.rp = reinterpret_cast<const uint4*>(g0);
+            L.ep = reinterpret_cast<const uint4*>(g0 + A.stage_recs * 16);
+        }
     }
     for (;;) { // phases, CTA-uniform
         ++L.epoch;
