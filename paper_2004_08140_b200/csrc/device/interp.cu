@@ -237,7 +237,7 @@ struct Lane : std::conditional_t<kM == 3, LaneRecs, LaneNoRecs> {
     static constexpr bool kCompact = kGC && kGcCompactVF;
     uint32_t vsh;    // kSmem: shared address of slot 0 (kCompact: its payload word)
     uint32_t vstr;   // kSmem: bytes from one slot to the next
-    uint32_t gsh;    // kCompact: shared address of slot 0's tag byte (32 bytes per slot)
+    uint32_t gsh;    // kCompact: tag byte of the payload word at a = (a >> 2) + gsh (CTA-uniform)
     // kTP: only SSA values and phi staging live in the lane's value file; the
     // parameters (per test) and literals (per variant) are CTA-shared tables
     uint32_t nv;     // kTP: n_values (slots below: lane value file)
@@ -303,11 +303,13 @@ struct Lane : std::conditional_t<kM == 3, LaneRecs, LaneNoRecs> {
     // kCompact: row of a lane-file slot (values, then phi staging)
     __device__ __forceinline__ uint2 V(uint32_t s) const {
         if (kCompact) {
-            if (!kTpTables)
-                return make_uint2(lds1(vsh + s * 128), ldsb(gsh + s * 32));
+            if (!kTpTables) {
+                const uint32_t a = vsh + s * 128;
+                return make_uint2(lds1(a), ldsb((a >> 2) + gsh));
+            }
             if (s < nv || s >= stage_base) {
-                const uint32_t row = s < nv ? s : nv + s - stage_base;
-                return make_uint2(lds1(vsh + row * 128), ldsb(gsh + row * 32));
+                const uint32_t a = vsh + (s < nv ? s : nv + s - stage_base) * 128;
+                return make_uint2(lds1(a), ldsb((a >> 2) + gsh));
             }
             return lds2(s < lit_begin ? tsh + (s - nv) * tstr : lsh + (s - lit_begin) * 8);
         }
@@ -320,12 +322,13 @@ struct Lane : std::conditional_t<kM == 3, LaneRecs, LaneNoRecs> {
     __device__ __forceinline__ void W(uint32_t s, uint32_t payload, uint32_t tag) {
         if (kCompact) {
             if (!kTpTables) {
-                sts1(vsh + s * 128, payload);
-                stsb(gsh + s * 32, tag);
+                const uint32_t a = vsh + s * 128;
+                sts1(a, payload);
+                stsb((a >> 2) + gsh, tag);
             } else if (s < nv || s >= stage_base) {
-                const uint32_t row = s < nv ? s : nv + s - stage_base;
-                sts1(vsh + row * 128, payload);
-                stsb(gsh + row * 32, tag);
+                const uint32_t a = vsh + (s < nv ? s : nv + s - stage_base) * 128;
+                sts1(a, payload);
+                stsb((a >> 2) + gsh, tag);
             } else {
                 sts2(s < lit_begin ? tsh + (s - nv) * tstr : lsh + (s - lit_begin) * 8, payload, tag);
             }
@@ -1645,8 +1648,32 @@ __device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread
                     break;
                 const float fx = __uint_as_float(x.x), fy = __uint_as_float(y.x);
                 uint32_t v, vt = otag;
-#ifndef GEVO_RUN_BRANCHY
-                {
+                // Branch-free: every cheap result is computed and op selects one
+                // (a switch, GEVO_RUN_BRANCHY, measured slower even where the
+                // reconvergence gate keeps the opcode warp-uniform)
+#ifdef GEVO_RUN_BRANCHY
+                constexpr bool kUniformOp = true;
+#else
+                constexpr bool kUniformOp = false; // (kGC measured 7-10 % slower on configs 3-4)
+#endif
+                if constexpr (kUniformOp) {
+                    switch (op) {
+                    case GEVO_OP_ADD: v = x.x + y.x; break;
+                    case GEVO_OP_SUB: v = x.x - y.x; break;
+                    case GEVO_OP_MUL: v = x.x * y.x; break;
+                    case GEVO_OP_FADD: v = __float_as_uint(__fadd_rn(fx, fy)); break;
+                    case GEVO_OP_FSUB: v = __float_as_uint(__fsub_rn(fx, fy)); break;
+                    case GEVO_OP_FMUL: v = __float_as_uint(__fmul_rn(fx, fy)); break;
+                    case GEVO_OP_ICMP:
+                        v = cmp(static_cast<int32_t>(x.x), static_cast<int32_t>(y.x), f_aux(r)) ? 1u : 0u;
+                        vt = GEVO_TAG_BOOL;
+                        break;
+                    default: // FCMP
+                        v = cmp(fx, fy, f_aux(r)) ? 1u : 0u;
+                        vt = GEVO_TAG_BOOL;
+                        break;
+                    }
+                } else {
                     // branch-free: every cheap result is computed and op selects
                     // one; a compare's predicate is a mask over (lt, eq, gt)
                     // plus an invert bit (ne = !eq, true when unordered)
@@ -1669,24 +1696,6 @@ __device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread
                     v = selp(is_cmp, c, selp(op <= GEVO_OP_MUL, vi, vf));
                     vt = selp(is_cmp, static_cast<uint32_t>(GEVO_TAG_BOOL), otag);
                 }
-#else
-                switch (op) {
-                case GEVO_OP_ADD: v = x.x + y.x; break;
-                case GEVO_OP_SUB: v = x.x - y.x; break;
-                case GEVO_OP_MUL: v = x.x * y.x; break;
-                case GEVO_OP_FADD: v = __float_as_uint(__fadd_rn(fx, fy)); break;
-                case GEVO_OP_FSUB: v = __float_as_uint(__fsub_rn(fx, fy)); break;
-                case GEVO_OP_FMUL: v = __float_as_uint(__fmul_rn(fx, fy)); break;
-                case GEVO_OP_ICMP:
-                    v = cmp(static_cast<int32_t>(x.x), static_cast<int32_t>(y.x), f_aux(r)) ? 1u : 0u;
-                    vt = GEVO_TAG_BOOL;
-                    break;
-                default: // FCMP
-                    v = cmp(fx, fy, f_aux(r)) ? 1u : 0u;
-                    vt = GEVO_TAG_BOOL;
-                    break;
-                }
-#endif
                 L.W(res, v, vt);
                 ++pc;
 #ifndef GEVO_RUN_BRANCHY
@@ -2419,7 +2428,9 @@ __device__ __forceinline__ void tp_item(const InterpArgs& A, TpInst& S, uint32_t
     if (Lane<kM>::kCompact) {
         L.vsh = sbase + (w * 32 * lane_slots + l) * 4;
         L.vstr = 32 * 4;
-        L.gsh = sbase + warps * 32 * lane_slots * 4 + w * 32 * lane_slots + l;
+        // tag array [warp][slot][lane] bytes after the payload words: the tag of
+        // the word at a is at tag0 + (a - sbase) / 4
+        L.gsh = sbase + warps * 32 * lane_slots * 4 - (sbase >> 2);
     } else {
         L.vsh = sbase + (w * 32 * lane_slots + l) * 8;
         L.vstr = 32 * 8;
