@@ -1854,7 +1854,9 @@ __device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread
             if ((th.executed >= S.next || S.mode != 0) && !th.slow)
                 spin_at_entry(A, L, th, S);
             pc = b.start + static_cast<uint32_t>(th.ip);
-            entered = true;
+            // lanes running together stay together through an unconditional
+            // branch; only a two-way one may split them (back to the gate)
+            entered = f_aux(r) == 2;
             return kStopNone;
         } else if (op == GEVO_OP_LOAD || op == GEVO_OP_STORE) {
 #ifndef GEVO_NO_MEM_FAST
@@ -1939,7 +1941,7 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
         bool run = true, together = true;
         if (gate && off) {
             --off;
-        } else if (gate) {
+        } else if (gate && (live & (live - 1))) { // (a lone live lane runs ungated)
             const int leader = __ffs(live) - 1;
             const uint32_t lead = follow ? __shfl_sync(live, pc, leader) : __reduce_min_sync(live, pc);
             run = pc == lead;
@@ -1962,11 +1964,13 @@ __device__ __forceinline__ int run_thread(const InterpArgs& A, Lane<kM>& L, Thre
         }
         if (run) {
             bool entered = false;
-            do
+            const bool lone = !(live & (live - 1)); // nothing to meet: run to the stop
+            do {
+                entered = false;
                 stop = run_unit(A, L, th, S, b, pc, code, first_fail, entered);
-            while (together && stop == kStopNone && !entered);
+            } while (together && stop == kStopNone && (!entered || lone));
         }
-        if (gate)
+        if (gate && (live & (live - 1)))
             live = __ballot_sync(live, stop == kStopNone);
         if (stop != kStopNone) {
             // a barrier ended the phase: an attempt in progress counts as a
