@@ -186,6 +186,12 @@ __device__ __forceinline__ uint32_t ldsb(uint32_t a) {
 __device__ __forceinline__ void stsb(uint32_t a, uint32_t x) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(x) : "memory");
 }
+// A value the compiler must keep rather than recompute.
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+    uint32_t y;
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
 __device__ __forceinline__ uint32_t lds1(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -2429,14 +2435,16 @@ __device__ __forceinline__ void tp_item(const InterpArgs& A, TpInst& S, uint32_t
 
     Lane<kM> L;
     L.gvf = nullptr;
+    // (vsh goes through an opaque move: rematerialising it from the thread
+    // index and the slot count at every value-file access cost ~9 SASS per IR)
     if (Lane<kM>::kCompact) {
-        L.vsh = sbase + (w * 32 * lane_slots + l) * 4;
+        L.vsh = opaque(sbase + (w * 32 * lane_slots + l) * 4);
         L.vstr = 32 * 4;
         // tag array [warp][slot][lane] bytes after the payload words: the tag of
         // the word at a is at tag0 + (a - sbase) / 4
         L.gsh = sbase + warps * 32 * lane_slots * 4 - (sbase >> 2);
     } else {
-        L.vsh = sbase + (w * 32 * lane_slots + l) * 8;
+        L.vsh = opaque(sbase + (w * 32 * lane_slots + l) * 8);
         L.vstr = 32 * 8;
         L.gsh = 0;
     }
