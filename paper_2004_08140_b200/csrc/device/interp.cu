@@ -1611,6 +1611,15 @@ __device__ __forceinline__ bool misc_op(const InterpArgs& A, Lane<kM>& L, const 
     }
 }
 
+// add/sub/mul, fadd/fsub/fmul, icmp, fcmp: the ops of a straight-line
+// arithmetic run (one bit test; op < 32 for every record)
+__device__ __forceinline__ bool plain_arith(uint32_t op) {
+    constexpr uint32_t kMask = (1u << GEVO_OP_ADD) | (1u << GEVO_OP_SUB) | (1u << GEVO_OP_MUL) |
+                               (1u << GEVO_OP_FADD) | (1u << GEVO_OP_FSUB) | (1u << GEVO_OP_FMUL) |
+                               (1u << GEVO_OP_ICMP) | (1u << GEVO_OP_FCMP);
+    return (kMask >> (op & 31u)) & 1u;
+}
+
 // One scheduling unit of a simulated thread at pc: a straight-line run of
 // plain arithmetic, one other instruction, or a branch with the entry of its
 // target block. Returns kStopNone to continue, else the stop kind.
@@ -1635,7 +1644,7 @@ __device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread
             }
         }
 #ifndef GEVO_NO_ARITH_RUN
-        else if (op <= GEVO_OP_FCMP && op != GEVO_OP_SDIV && op != GEVO_OP_FDIV) {
+        else if (plain_arith(op)) {
             // Straight-line run of plain arithmetic (block-level charging, no
             // abstract iterate): a tight loop in which only pc and the record
             // are live. It stops at the first instruction it does not handle
@@ -1710,7 +1719,7 @@ __device__ __forceinline__ int run_unit(const InterpArgs& A, Lane<kM>& L, Thread
                 r = L.rec(pc);
 #endif
                 op = f_op(r);
-                if (op > GEVO_OP_FCMP || op == GEVO_OP_SDIV || op == GEVO_OP_FDIV)
+                if (!plain_arith(op))
                     break;
             }
         }
