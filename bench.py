@@ -261,6 +261,19 @@ def issue_profile(workload):
     return prof.get("workloads", {}).get(workload)
 
 
+def useful_ir_fraction(v, t):
+    """Reference-equivalent instructions of the tests the reference runs (each
+    variant's tests up to its first failing one; all of them when it passes) /
+    those of every test the device ran, from one pass with per-test records."""
+    import numpy as np
+    ir = t["ir"].astype(np.float64)
+    ff = v["failing_test"].astype(np.int64)
+    idx = np.arange(ir.shape[1])[None, :]
+    ref_run = (ff[:, None] < 0) | (idx <= ff[:, None])
+    total = float(ir.sum())
+    return float(ir[ref_run].sum()) / total if total > 0 else None
+
+
 def roofline_of(workload, step_ms, f_mhz, ir_ref_step, ir_dev_step):
     """Issue-slot roofline: the interpreter is integer dispatch
     with per-test working sets on chip. achieved = SASS warp instructions the
@@ -379,6 +392,7 @@ def b200_arm(args):
     # excluded, speculative tests / aborted threads / re-runs included
     ir_dev_step = gevo.work_counters(reset=True)
     spins = gevo.spin_counters(reset=True)
+    useful = useful_ir_fraction(v, t)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
@@ -482,6 +496,12 @@ def b200_arm(args):
     ck = clocks.summary()
     f_mhz = ck["sm_mhz"] or 1965.0
     roofline = roofline_of("config4", dev_ms / args.steps, f_mhz, ir_ref_step, ir_dev_step)
+    if roofline.get("frac") is not None and useful is not None:
+        # the share of the step's work the reference also does: tests up to and
+        # including each variant's first failing test (the rest is speculative
+        # work early exit discards), in reference-equivalent instructions
+        roofline["useful_ir_frac"] = useful
+        roofline["useful_frac"] = roofline["frac"] * useful
     roofline["lib_ms_per_step"] = statistics.mean(lib_ms) if lib_ms else None
 
     cpu = None
