@@ -592,7 +592,11 @@ def secondary_config2(args, gevo, torch, stream, flush, c2, barrier, world):
         "e2e": {"value": execs * world / (statistics.mean(e2e_steps) / 1e3), "unit": UNIT},
         "ir_per_s": ir_ref * world / (ms / 1e3),
         "executions_per_step": execs * world,
-        "batch_live_ms_max": round(max(live), 4),
+        # per step: the longest batch's own device span next to the step's
+        # window (the batches run inside the window: live <= step)
+        "step_ms": [round(x, 4) for x in steps],
+        "batch_live_ms": [round(x, 4) for x in live],
+        "live_within_step": all(l <= s + 1e-3 for l, s in zip(live, steps)),
         "roofline": roofline_of("config2", ms, 1965.0, ir_ref, None),
     }
 
